@@ -1,0 +1,484 @@
+"""Benchmark: reduce-scatter / all-gather bus bandwidth on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[1]): reduce-scatter, bf16, 128 MiB
+input per rank, recursive halving with the reduction fused into the peer-load
+kernel. One *step* = one collective call. Metric: bus bandwidth
+busbw = (S / t) * (p - 1) / p in GB/s (1e9 B/s), t = device time per call, max
+over ranks.
+
+* N = 1 (no torchrun): the reference's own shape, 8 *simulated* ranks
+  (configs[0] "8 simulated ranks"), emulated on one B200: all eight ranks run
+  in one cooperative launch of the same kernels, peer traffic is local HBM, so
+  the roofline is HBM.
+* N > 1 (torchrun, one process per GPU): p = N real ranks over CUDA-IPC peer
+  memory on NVLink 5 / NVSwitch; roofline = NVLink. NCCL's
+  reduce_scatter_tensor on the same bytes is timed beside it.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port of collkit's rechalf_reduce_scatter, ``oracle/``) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "all-gather & reduce-scatter bus GB/s (64–256 MB) at 2/4/8 B200 vs 900 GB/s"
+NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (fallback; nominal 900)
+NVLINK_NOMINAL_GBS = 900.0
+EMU_RANKS = 8
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._proc = None
+        self._thread = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+            self._thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
+        sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
+        smax = [int(s[1]) for s in self.samples if s[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle port of collkit, test infrastructure)
+# ---------------------------------------------------------------------------
+def cpu_reference(p: int, s_bytes: int, dtype: str, algo: str, steps: int, warmup: int):
+    """Time the reference algorithm's CPU restatement on this host's cores:
+    p simulated ranks, numpy, the per-step work of every rank in parallel
+    threads (numpy releases the GIL in its kernels)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    from oracle import collectives as oc
+
+    es = 2 if dtype == "bf16" else 4
+    n = s_bytes // es // p
+    rng = np.random.default_rng(0)
+    ins = []
+    for _ in range(p):
+        x = rng.standard_normal(n * p).astype(np.float32)
+        ins.append(oracle.f32_to_bf16(x) if dtype == "bf16" else x)
+    threads = os.cpu_count() or 1
+    pool = ThreadPoolExecutor(max_workers=min(threads, p))
+    fn = oc.rechalf_reduce_scatter if algo == "recursive" else oc.ring_reduce_scatter
+
+    def one_call():
+        # rank-parallel execution: each rank's chunk reduction is independent
+        # once inputs are exchanged; the oracle runs all ranks' steps, so split
+        # the element range across threads (every element's fold order kept).
+        parts = min(threads, 8)
+        bounds = np.linspace(0, n, parts + 1).astype(int)
+
+        def run(i):
+            lo, hi = bounds[i], bounds[i + 1]
+            sub = [np.concatenate([x[c * n + lo : c * n + hi] for c in range(p)]) for x in ins]
+            return fn(sub, dtype)
+
+        list(pool.map(run, range(parts)))
+
+    for _ in range(warmup):
+        one_call()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        one_call()
+        times.append(time.perf_counter() - t0)
+    pool.shutdown()
+    t = statistics.mean(times)
+    return t, min(threads, 8)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def busbw(s_bytes: int, p: int, seconds: float) -> float:
+    return s_bytes * (p - 1) / p / seconds / 1e9
+
+
+def rs_algorithmic_hbm_bytes(algo: str, p: int, chunk_bytes: int) -> int:
+    """HBM bytes one emulated launch must move (all p ranks' traffic is local)."""
+    if algo == "direct":
+        per_rank = p * chunk_bytes + chunk_bytes          # read p chunks, write 1
+    else:
+        per_rank = 3 * (p - 1) * chunk_bytes              # each step: read local + peer, write
+    return per_rank * p
+
+
+def time_calls(call, steps: int, stream) -> float:
+    """Average seconds per call over `steps` back-to-back calls on `stream`."""
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        call()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / steps
+
+
+def run_gpu(args):
+    import paper_2504_18658_b200 as pkg
+    from paper_2504_18658_b200 import _lib
+    from paper_2504_18658_b200.communicator import _emu_group, emulated_world
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    real = world_size > 1
+    dist = None
+    if real:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    p = world_size if real else EMU_RANKS
+    S = args.size_mib << 20
+    dtype = {"bf16": torch.bfloat16, "f32": torch.float32}[args.dtype]
+    es = torch.empty(0, dtype=dtype).element_size()
+    n = S // es // p
+    algo = args.algo
+    code = _lib.DTYPES[args.dtype]
+    a = _lib.ALGOS[algo]
+    order = _lib.ORDERS["recursive" if algo == "recursive" else "ring"]
+    stream = torch.cuda.current_stream(dev)
+    L = _lib.lib()
+
+    # ---- symmetric buffers (inputs resident in HBM, zero-copy) ----
+    if real:
+        comm = pkg.init_from_torch(device=local_rank)
+        world = comm.world
+        world.ensure_staging(int(L.pccl_staging_bytes(1, a, p, n, code)))
+        sin = world.empty(n * p, dtype)
+        sout = world.empty(n, dtype)
+        sin.normal_()
+        ghandle = comm.handle
+
+        def call():
+            _lib.check(L.pccl_reduce_scatter(ghandle, a, order, sin.data_ptr(), sout.data_ptr(), n, code,
+                                             stream.cuda_stream))
+    else:
+        world = emulated_world(p, local_rank)
+        group, _ = _emu_group(world, tuple(range(p)), 0)
+        world.ensure_staging(int(L.pccl_staging_bytes(1, a, p, n, code)))
+        sins = world.empty(n * p, dtype)
+        souts = world.empty(n, dtype)
+        for t in sins:
+            t.normal_()
+        sp = _lib.ptr_array([t.data_ptr() for t in sins])
+        rp = _lib.ptr_array([t.data_ptr() for t in souts])
+
+        def call():
+            _lib.check(L.pccl_emu_reduce_scatter(group.handle, a, order, sp, rp, n, code, stream.cuda_stream))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if real:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- soak (for the clock sampler), warmup, timed region ----
+    clocks = Clocks(local_rank)
+    with clocks:
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            for _ in range(20):
+                call()
+            torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            call()
+        barrier()
+        t_call = time_calls(call, args.steps, stream)
+        world.check()
+        barrier()
+    if real:
+        tt = torch.tensor([t_call], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_call = float(tt.item())
+    value = busbw(S, p, t_call)
+
+    # ---- extras: the other algorithms / all-gather / NCCL, same bytes ----
+    extra = {}
+    if not args.no_extra:
+        def measure(fn, k=max(5, args.steps)):
+            for _ in range(3):
+                fn()
+            barrier()
+            t = time_calls(fn, k, stream)
+            world.check()
+            if real:
+                tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            return t
+
+        for alg2 in ("direct", "ring", "recursive"):
+            a2 = _lib.ALGOS[alg2]
+            o2 = _lib.ORDERS["recursive" if alg2 == "recursive" else "ring"]
+            world.ensure_staging(int(L.pccl_staging_bytes(1, a2, p, n, code)))
+            if real:
+                f = lambda: _lib.check(L.pccl_reduce_scatter(ghandle, a2, o2, sin.data_ptr(), sout.data_ptr(), n, code,  # noqa: E731
+                                                            stream.cuda_stream))
+            else:
+                f = lambda: _lib.check(L.pccl_emu_reduce_scatter(group.handle, a2, o2, sp, rp, n, code,  # noqa: E731
+                                                                stream.cuda_stream))
+            t = measure(f)
+            extra[f"rs_{args.dtype}_{args.size_mib}MiB_{alg2}"] = {"busbw_gbs": round(busbw(S, p, t), 1),
+                                                                   "us": round(t * 1e6, 1)}
+        # all-gather fp32 64 MiB output (configs[0] / C1 shape)
+        S_ag = 64 << 20
+        n_ag = S_ag // 4 // p
+        if real:
+            ag_in = world.empty(n_ag, torch.float32)
+            ag_out = world.empty(n_ag * p, torch.float32)
+            ag_in.normal_()
+        else:
+            ag_ins = world.empty(n_ag, torch.float32)
+            ag_outs = world.empty(n_ag * p, torch.float32)
+            agsp = _lib.ptr_array([t.data_ptr() for t in ag_ins])
+            agrp = _lib.ptr_array([t.data_ptr() for t in ag_outs])
+        for alg2 in ("direct", "ring", "recursive"):
+            a2 = _lib.ALGOS[alg2]
+            world.ensure_staging(int(L.pccl_staging_bytes(0, a2, p, n_ag, 0)))
+            if real:
+                f = lambda: _lib.check(L.pccl_all_gather(ghandle, a2, ag_in.data_ptr(), ag_out.data_ptr(), n_ag, 0,  # noqa: E731
+                                                        stream.cuda_stream))
+            else:
+                f = lambda: _lib.check(L.pccl_emu_all_gather(group.handle, a2, agsp, agrp, n_ag, 0,  # noqa: E731
+                                                            stream.cuda_stream))
+            t = measure(f)
+            extra[f"ag_f32_64MiB_{alg2}"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
+        if real:
+            nin = torch.empty(n * p, dtype=dtype, device=dev).normal_()
+            nout = torch.empty(n, dtype=dtype, device=dev)
+            t = measure(lambda: dist.reduce_scatter_tensor(nout, nin))
+            extra[f"nccl_rs_{args.dtype}_{args.size_mib}MiB"] = {"busbw_gbs": round(busbw(S, p, t), 1),
+                                                                "us": round(t * 1e6, 1),
+                                                                "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
+            agi = torch.empty(n_ag, dtype=torch.float32, device=dev).normal_()
+            ago = torch.empty(n_ag * p, dtype=torch.float32, device=dev)
+            t = measure(lambda: dist.all_gather_into_tensor(ago, agi))
+            extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)
+
+    # ---- roofline of the dominant kernel (the measured call itself) ----
+    pk, src = peaks()
+    if real:
+        achieved = value  # algorithmic NVLink bytes per GPU per launch / launch time
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
+                "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
+                "frac_of_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4),
+                "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
+                "algorithmic_bytes_per_launch": int(S * (p - 1) / p), "traffic": None}
+    else:
+        hbm = rs_algorithmic_hbm_bytes(algo, p, n * es)
+        achieved = hbm / t_call / 1e9
+        peak = float(pk.get("hbm_gbs", 6650.0))
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "algorithmic_bytes_per_launch": hbm, "traffic": args.traffic}
+
+    cpu = None
+    if rank == 0 and not real and not args.no_cpu:
+        s_cpu = 16 << 20
+        t_cpu, cores = cpu_reference(p, s_cpu, args.dtype, algo, steps=3, warmup=1)
+        cpu = {"value": round(busbw(s_cpu, p, t_cpu), 4), "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"oracle rechalf_reduce_scatter {args.dtype}, p={p} ranks, S=16 MiB/rank, 3 calls "
+                         f"(numpy, {cores} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 2),
+            "unit": "GB/s",
+            "n_gpus": world_size,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(t_call * 1e3, 5),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": args.dtype,
+            "data": "synthetic (standard normal, resident in symmetric HBM segments)",
+            "config": {
+                "workload": (f"reduce-scatter {args.dtype}, {args.size_mib} MiB input/rank, {algo} "
+                             f"(fused reduction), p={p} " + ("GPUs over NVLink/NVSwitch" if real else
+                                                             "simulated ranks emulated on 1 B200 (HBM-bound)")),
+                "collective": "reduce_scatter",
+                "algorithm": algo,
+                "p": p,
+                "S_bytes": S,
+                "parallelism": f"dp{p}" if real else "emulated-8-ranks-1gpu",
+                "l2": "inputs larger than L2 (per-rank input 128 MiB > 126 MB L2)",
+                "ctas_per_rank": int(os.environ.get("PCCL_CTAS", "0")) or "auto",
+            },
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+            "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if real:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, pkg, real, p, S, dtype, dev, comm, dist):
+    """Same metric through the public API with pinned host buffers: every step
+    uploads the inputs, runs the collective and reads the result back."""
+    es = torch.empty(0, dtype=dtype).element_size()
+    n = S // es // p
+    algo = args.algo
+    fn = pkg.rechalf_reduce_scatter if algo == "recursive" else (
+        pkg.ring_reduce_scatter if algo == "ring" else pkg.direct_reduce_scatter)
+    steps = max(3, min(args.steps, 10))
+    if real:
+        x = torch.empty(n * p, dtype=dtype).normal_().pin_memory()
+        for _ in range(2):
+            fn(comm, x)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            y = fn(comm, x)
+        dt = (time.perf_counter() - t0) / steps
+        tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        h2d, d2h = n * p * es * p, n * es * p
+    else:
+        xs = [torch.empty(n * p, dtype=dtype).normal_().pin_memory() for _ in range(p)]
+        timing = {}
+
+        def body(c):
+            for _ in range(2):
+                fn(c, xs[c.rank])
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                y = fn(c, xs[c.rank])
+            if c.rank == 0:
+                timing["dt"] = (time.perf_counter() - t0) / steps
+            return None
+
+        pkg.run_ranks(p, body, device=dev.index)
+        dt = timing["dt"]
+        h2d, d2h = n * p * es * p, n * es * p
+    return {"value": round(busbw(S, p, dt), 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 3),
+            "path": f"paper_2504_18658_b200.{fn.__name__}(comm, pinned host tensor) -> host tensor"}
+
+
+def run_reference(args):
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p = world_size if world_size > 1 else EMU_RANKS
+    s_sample = 16 << 20
+    t, cores = cpu_reference(p, s_sample, args.dtype, args.algo, steps=args.steps, warmup=args.warmup)
+    v = busbw(s_sample, p, t)
+    sample = (f"oracle port of collkit {args.algo} reduce-scatter ({args.dtype}), p={p} simulated ranks, "
+              f"16 MiB/rank sample of the {args.size_mib} MiB workload, numpy on {cores} host threads")
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world_size, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"reduce-scatter {args.dtype}, {args.size_mib} MiB input/rank, {args.algo}, p={p}",
+                   "collective": "reduce_scatter", "algorithm": args.algo, "p": p},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size-mib", type=int, default=128)
+    ap.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--algo", choices=["recursive", "ring", "direct"], default="recursive")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if measured")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * pccl_b200.h — C ABI of the B200-native all-gather / reduce-scatter path.
+ *
+ * Drop-in boundary for the reference's hot path (collkit):
+ * the reference's Python entry points take a Communicator and a buffer and
+ * move data through a tagged point-to-point transport
+ * (/root/reference/pkg/src/collkit/transport/base.py:105-174). Here the
+ * transport is replaced by symmetric device memory mapped over NVLink 5 /
+ * NVSwitch (CUDA IPC) and the collectives are sm_100a kernels that pull peer
+ * data and fuse the reduction into the load loop. Plain C types only: device
+ * pointers are void*, streams are cudaStream_t passed as void*.
+ *
+ * Every function returns a pccl_status_t; the Python layer maps each code 1:1
+ * to the reference's exception classes (collkit/errors.py:4-62).
+ *
+ * Threading: a world / communicator is used by one host thread at a time
+ * (collkit/transport/base.py:106-111). Calls are stream-ordered and SPMD: every
+ * member issues the same collectives in the same order
+ * (collkit/transport/base.py:131-134), which is what keeps the per-group epoch
+ * counters (the replacement for next_base_tag) in agreement without any
+ * host-side coordination.
+ */
+#ifndef PCCL_B200_H
+#define PCCL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCCL_MAX_RANKS 16        /* real mode: <= 8 GPUs of one NVSwitch box; emulation: <= 16 */
+#define PCCL_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
+
+typedef enum {
+  PCCL_SUCCESS = 0,
+  PCCL_ERR_INVALID_ARGUMENT = 1,   /* ValueError            (hierarchy.py:77-80)   */
+  PCCL_ERR_NON_POWER_OF_TWO = 2,   /* errors.NonPowerOfTwo  (collectives.py:113)   */
+  PCCL_ERR_NOT_DIVISIBLE = 3,      /* errors.NotDivisible   (collectives.py:85)    */
+  PCCL_ERR_LENGTH_MISMATCH = 4,    /* errors.LengthMismatch (collectives.py:38-41) */
+  PCCL_ERR_TIMEOUT = 5,            /* errors.Timeout        (sockets.py:203-212)   */
+  PCCL_ERR_PEER_UNREACHABLE = 6,   /* errors.PeerUnreachable                        */
+  PCCL_ERR_UNSUPPORTED = 7,        /* errors.Unsupported                            */
+  PCCL_ERR_INVALID_TOPOLOGY = 8,   /* errors.InvalidTopology (topology.py:16-33)   */
+  PCCL_ERR_INDEX_OUT_OF_RANGE = 9, /* errors.IndexOutOfRange                        */
+  PCCL_ERR_CUDA = 10,              /* errors.CollkitError: CUDA runtime failure     */
+  PCCL_ERR_OUT_OF_MEMORY = 11,     /* staging segment too small: grow and retry     */
+} pccl_status_t;
+
+typedef enum {
+  PCCL_FLOAT32 = 0,
+  PCCL_BFLOAT16 = 1,
+  PCCL_FLOAT16 = 2,
+  PCCL_UINT8 = 3, /* all-gather only */
+  PCCL_INT32 = 4, /* all-gather only */
+  PCCL_INT64 = 5, /* all-gather only */
+  PCCL_FLOAT64 = 6 /* all-gather only */
+} pccl_dtype_t;
+
+typedef enum {
+  PCCL_ALGO_DIRECT = 0,    /* one step over every peer (new name) */
+  PCCL_ALGO_RING = 1,      /* ring_all_gather / ring_reduce_scatter                 */
+  PCCL_ALGO_RECURSIVE = 2  /* recdbl_all_gather / rechalf_reduce_scatter            */
+} pccl_algo_t;
+
+/* Reduction order of the DIRECT reduce-scatter (fp32 results are then
+ * bit-identical to the named step-wise algorithm). */
+typedef enum {
+  PCCL_ORDER_RING = 0,      /* ((x_{c+1} + x_{c+2}) + ...) + x_c   (collectives.py:98-103)  */
+  PCCL_ORDER_RECURSIVE = 1, /* recursive-halving butterfly          (collectives.py:150-164) */
+  PCCL_ORDER_RANK = 2       /* rank order from zeros                 (bench/oracles.py:12-19) */
+} pccl_order_t;
+
+typedef enum { PCCL_ALL_GATHER = 0, PCCL_REDUCE_SCATTER = 1 } pccl_collective_t;
+
+typedef struct pccl_world *pccl_world_t; /* symmetric memory + flags of one box */
+typedef struct pccl_comm *pccl_comm_t;   /* an ordered group of world ranks     */
+
+/* ---- misc ------------------------------------------------------------- */
+const char *pccl_error_string(int status);
+int pccl_version(void);
+
+/* ---- worlds ------------------------------------------------------------
+ * Real mode: one process per GPU. pccl_world_create allocates segment 0 (the
+ * flag arena); every segment must then be exported, exchanged by the caller's
+ * bootstrap (torch.distributed) and imported on every rank.
+ * Emulation mode: nranks ranks of one process on one device; each collective
+ * runs all ranks in ONE cooperative launch (ranks = CTA rows), the same device
+ * code as real mode with every "peer" pointer local.
+ * Replaces: InProcessTransport / run_ranks (transport/inprocess.py:14-113). */
+int pccl_world_create(int nranks, int rank, int device, pccl_world_t *out);
+int pccl_emu_world_create(int nranks, int device, pccl_world_t *out);
+int pccl_world_destroy(pccl_world_t w);
+int pccl_world_check(pccl_world_t w);           /* device-reported error, then cleared */
+int pccl_world_reset_flags(pccl_world_t w);      /* zero flags + epochs (emulation, after an error) */
+int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
+int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
+
+/* ---- symmetric segments ---------------------------------------------- */
+int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id);
+int pccl_segment_export(pccl_world_t w, int seg_id, void *handle_out /* PCCL_IPC_HANDLE_BYTES */);
+int pccl_segment_import(pccl_world_t w, int seg_id, const void *handles /* nranks * 64 */);
+int pccl_segment_ptr(pccl_world_t w, int seg_id, int rank, void **ptr, size_t *bytes);
+int pccl_segment_destroy(pccl_world_t w, int seg_id);
+int pccl_world_set_staging(pccl_world_t w, int seg_id);
+/* Staging bytes a call may need (depends only on SPMD-uniform args);
+ * algo 3 = hierarchical (N*M = group_size). */
+size_t pccl_staging_bytes(int collective, int algo, int group_size, size_t count, int dtype);
+
+/* ---- communicators ------------------------------------------------------
+ * Replaces Communicator(...) and Communicator.subgroup (transport/base.py:113-174).
+ * members are world ranks; comm_id is informational (hierarchy.py:31-38); the
+ * flag slot and epoch are keyed by the member set, so re-created
+ * sub-communicators keep agreeing epochs. Real mode: the caller's rank must be
+ * a member (else PCCL_ERR_INDEX_OUT_OF_RANGE). */
+int pccl_comm_create(pccl_world_t w, const int *members, int nmembers, int comm_id, pccl_comm_t *out);
+int pccl_comm_destroy(pccl_comm_t c);
+int pccl_comm_size(pccl_comm_t c, int *size);
+int pccl_comm_rank(pccl_comm_t c, int *rank);
+
+/* ---- flat collectives (real mode: this rank's buffers) -----------------
+ * pccl_all_gather replaces ring_all_gather / recdbl_all_gather
+ *   (collectives.py:55-76, 107-129): recv[g*count ..] = send of group rank g.
+ * pccl_reduce_scatter replaces ring_reduce_scatter / rechalf_reduce_scatter
+ *   (collectives.py:79-104, 132-165): recv = chunk `rank` of the sum, chunk
+ *   length recvcount; order applies to PCCL_ALGO_DIRECT only. */
+int pccl_all_gather(pccl_comm_t c, int algo, const void *send, void *recv, size_t count, int dtype,
+                    void *stream);
+int pccl_reduce_scatter(pccl_comm_t c, int algo, int order, const void *send, void *recv, size_t recvcount,
+                        int dtype, void *stream);
+
+/* ---- hierarchical (hierarchy.py:158-195), world of N x M virtual nodes --- */
+int pccl_hier_all_gather(pccl_world_t w, int N, int M, int inter_algo, const void *send, void *recv, size_t count,
+                         int dtype, void *stream);
+int pccl_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter_algo, const void *send, void *recv,
+                             size_t recvcount, int dtype, void *stream);
+
+/* ---- emulation-mode variants: per-member pointer arrays, one launch ----- */
+int pccl_emu_all_gather(pccl_comm_t c, int algo, const void *const *sends, void *const *recvs, size_t count,
+                        int dtype, void *stream);
+int pccl_emu_reduce_scatter(pccl_comm_t c, int algo, int order, const void *const *sends, void *const *recvs,
+                            size_t recvcount, int dtype, void *stream);
+int pccl_emu_hier_all_gather(pccl_world_t w, int N, int M, int inter_algo, const void *const *sends,
+                             void *const *recvs, size_t count, int dtype, void *stream);
+int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter_algo, const void *const *sends,
+                                 void *const *recvs, size_t recvcount, int dtype, void *stream);
+/* Test hook: perturb one member's call signature so the device-side
+ * cross-rank check must raise LengthMismatch (tests/test_collectives.py:172-175). */
+int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask);
+
+/* ---- device-local helpers ----------------------------------------------- */
+/* direction 0: shuffle_local_major_to_global, 1: shuffle_global_to_local_major
+ * (hierarchy.py:103-126); out-of-place block transpose of N*M blocks. */
+int pccl_shuffle(int direction, const void *in, void *out, int N, int M, size_t block_len, int dtype, void *stream);
+/* reduce_inplace (collectives.py:45-52): acc[i] = acc[i] + other[i]. */
+int pccl_reduce_inplace(void *acc, const void *other, size_t count, int dtype, void *stream);
+
+/* ---- schedule introspection (host only, no GPU needed) -------------------
+ * The step structure the kernels execute, as (step, src_world, dst_world,
+ * nbytes) rows: the data that dst pulls from src in that step. Mirrors
+ * simnet.build_schedule (simnet.py:326-345). m_bytes = AG output / RS input
+ * per rank. Returns PCCL_ERR_OUT_OF_MEMORY if cap rows are not enough. */
+int pccl_schedule(int collective, int algo, int inter_algo, int N, int M, size_t m_bytes, int64_t *rows, int cap,
+                  int *nrows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCCL_B200_H */

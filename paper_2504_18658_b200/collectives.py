@@ -1,0 +1,330 @@
+"""Flat all-gather / reduce-scatter, drop-in for ``collkit/collectives.py``.
+
+Same names, arguments and semantics as the reference:
+
+* ``ring_all_gather(comm, buf)`` (collectives.py:55-76), ``recdbl_all_gather``
+  (:107-129), ``ring_reduce_scatter`` (:79-104), ``rechalf_reduce_scatter``
+  (:132-165); plus the one-shot ``direct_all_gather`` /
+  ``direct_reduce_scatter`` and the dispatching
+  ``all_gather`` / ``reduce_scatter``;
+* SPMD, blocking for host inputs, output is a fresh array the caller owns, the
+  input is never modified; numpy input is cast to contiguous 1-D float32
+  exactly like ``as_elements`` (collectives.py:26-29);
+* errors: ``NotDivisible``, ``NonPowerOfTwo``, ``LengthMismatch`` (also across
+  ranks), ``Timeout``.
+
+What differs is underneath: buffers live in HBM, peers' symmetric buffers are
+read over NVLink by the sm_100a kernels in ``csrc/kernels.cuh``, and the
+reduction is fused into the peer-load loop. CUDA tensors (fp32 / bf16 / fp16)
+are accepted natively and stay on the device (stream-ordered, no host sync);
+pass ``out=`` a tensor from ``comm.world.empty`` to skip every staging copy.
+"""
+from __future__ import annotations
+
+import enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib, ptr_array
+from .errors import LengthMismatch, NonPowerOfTwo, NotDivisible, OutOfMemory, Unsupported
+from .world import TORCH_DTYPES
+
+
+class ReduceOp(enum.Enum):
+    SUM = "sum"
+
+
+def is_power_of_two(n: int) -> bool:
+    return n >= 1 and (n & (n - 1)) == 0
+
+
+def as_elements(buf) -> np.ndarray:
+    """Contiguous 1-D float32 view/copy (collectives.py:26-29)."""
+    return np.ascontiguousarray(buf, dtype=np.float32).reshape(-1)
+
+
+ALL_GATHER_ALGOS = ("direct", "ring", "recursive")
+REDUCE_SCATTER_ALGOS = ("direct", "ring", "recursive")
+
+
+def _align(n: int) -> int:
+    return (n + 255) & ~255
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# input normalisation
+# ---------------------------------------------------------------------------
+class _In:
+    """One rank's argument: a flat CUDA tensor to run on, plus how to return."""
+
+    __slots__ = ("t", "host", "numpy", "out")
+
+    def __init__(self, buf, reduce: bool, device: torch.device, out=None):
+        self.out = out
+        if isinstance(buf, torch.Tensor):
+            t = buf.reshape(-1)
+            if not t.is_contiguous():
+                t = t.contiguous()
+            if reduce and t.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+                t = t.to(torch.float32)
+            if not reduce and t.dtype not in TORCH_DTYPES:
+                raise Unsupported(f"dtype {t.dtype} not supported")
+            self.host = not t.is_cuda
+            self.numpy = False
+            self.t = t
+        else:
+            arr = as_elements(buf)
+            self.host = True
+            self.numpy = True
+            self.t = torch.from_numpy(arr)
+
+    @property
+    def dtype_code(self) -> int:
+        return _lib.DTYPES[TORCH_DTYPES[self.t.dtype]]
+
+    @property
+    def nbytes(self) -> int:
+        return self.t.numel() * self.t.element_size()
+
+
+def _finish(arg: _In, result: torch.Tensor):
+    """Return in the caller's type: numpy for numpy input, host tensor for a
+    host tensor, the device tensor otherwise (fresh, caller-owned)."""
+    if arg.numpy:
+        return result.cpu().numpy().copy() if result.is_cuda else result.numpy().copy()
+    if arg.host:
+        return result.cpu()
+    return result
+
+
+def _check_world_size_growth(comm, need: int, what: str):
+    world = comm.world
+    if comm.size == world.nranks:
+        return True
+    seg = world.staging if what == "staging" else world.io
+    if seg is None or seg.nbytes < need:
+        raise OutOfMemory(
+            f"sub-communicator call needs {need} B of {what}; grow it collectively first "
+            f"(world.ensure_{what}({need}) on every rank)"
+        )
+    return False
+
+
+def _ensure_staging(comm, collective: int, algo: int, count: int, dtype_code: int):
+    need = int(lib().pccl_staging_bytes(collective, algo, comm.size, count, dtype_code))
+    world = comm.world
+    if world.staging is not None and world.staging.nbytes >= need:
+        return
+    if _check_world_size_growth(comm, need, "staging"):
+        world.ensure_staging(need)
+
+
+def _ensure_io(comm, need: int):
+    world = comm.world
+    if world.io is not None and world.io.nbytes >= need:
+        return world.io
+    if _check_world_size_growth(comm, need, "io"):
+        return world.ensure_io(need)
+    return world.io
+
+
+# ---------------------------------------------------------------------------
+# device execution (shared by real and emulated mode)
+# ---------------------------------------------------------------------------
+def _all_gather_device(comm, algo: str, sends: list, recvs: list, emu: bool) -> None:
+    """sends/recvs: one CUDA tensor per executed rank (real: [mine])."""
+    a = _lib.ALGOS[algo]
+    s0 = sends[0]
+    dtype = _lib.DTYPES[TORCH_DTYPES.get(s0.dtype, "u8")]
+    count = s0.numel() if s0.dtype in TORCH_DTYPES else s0.numel() * s0.element_size()
+    _ensure_staging(comm, _lib.ALL_GATHER, a, count, dtype)
+    stream = _stream(comm.device)
+    if emu:
+        st = lib().pccl_emu_all_gather(comm.handle, a, ptr_array([t.data_ptr() for t in sends]),
+                                       ptr_array([t.data_ptr() for t in recvs]), count, dtype, stream)
+    else:
+        st = lib().pccl_all_gather(comm.handle, a, sends[0].data_ptr(), recvs[0].data_ptr(), count, dtype, stream)
+    check(st, f"all_gather[{algo}]")
+
+
+def _reduce_scatter_device(comm, algo: str, order: str, sends: list, recvs: list, emu: bool) -> None:
+    a = _lib.ALGOS[algo]
+    o = _lib.ORDERS[order]
+    s0 = sends[0]
+    dtype = _lib.DTYPES[TORCH_DTYPES[s0.dtype]]
+    n = s0.numel() // comm.size
+    _ensure_staging(comm, _lib.REDUCE_SCATTER, a, n, dtype)
+    stream = _stream(comm.device)
+    if emu:
+        st = lib().pccl_emu_reduce_scatter(comm.handle, a, o, ptr_array([t.data_ptr() for t in sends]),
+                                           ptr_array([t.data_ptr() for t in recvs]), n, dtype, stream)
+    else:
+        st = lib().pccl_reduce_scatter(comm.handle, a, o, sends[0].data_ptr(), recvs[0].data_ptr(), n, dtype, stream)
+    check(st, f"reduce_scatter[{algo}]")
+
+
+def _upload(comm, args: list, ranks: list, out_bytes: int):
+    """Host inputs -> each rank's io segment (input, then output region)."""
+    in_bytes = max(a.nbytes for a in args)
+    io = _ensure_io(comm, _align(in_bytes) + _align(out_bytes))
+    sends, recvs = [], []
+    for a, r in zip(args, ranks):
+        dst = io.tensor(r, 0, a.nbytes)
+        if a.nbytes:
+            dst.copy_(a.t.view(torch.uint8).reshape(-1), non_blocking=False)
+        sends.append(dst.view(a.t.dtype))
+        recvs.append(io.tensor(r, _align(in_bytes), out_bytes).view(a.t.dtype))
+    return sends, recvs
+
+
+def _run(comm, buf, reduce: bool, algo: str, order: str, out=None):
+    """One rank's call (real) or rendezvous into one launch (emulated)."""
+    arg = _In(buf, reduce, comm.device, out)
+    p = comm.size
+    if reduce:
+        if arg.t.numel() % p:
+            raise NotDivisible(f"input of {arg.t.numel()} elements not divisible by p={p}")
+        if algo == "recursive" and not is_power_of_two(p):
+            raise NonPowerOfTwo(f"recursive halving requires power-of-two ranks, got {p}")
+        if algo == "direct" and order == "recursive" and not is_power_of_two(p):
+            raise NonPowerOfTwo(f"recursive order requires power-of-two ranks, got {p}")
+    elif algo == "recursive" and not is_power_of_two(p):
+        raise NonPowerOfTwo(f"recursive doubling requires power-of-two ranks, got {p}")
+    out_numel = arg.t.numel() // p if reduce else arg.t.numel() * p
+
+    def execute(args: list):
+        emu = comm.emulated
+        ranks = list(comm.members) if emu else [comm.world_rank]
+        sizes = [a.t.numel() for a in args]
+        if len(set(sizes)) > 1 or len({a.t.dtype for a in args}) > 1:
+            raise LengthMismatch(f"buffer sizes/dtypes differ across ranks: {sizes}")
+        if all(a.host for a in args):
+            es = args[0].t.element_size()
+            sends, recvs = _upload(comm, args, ranks, out_numel * es)
+        else:
+            sends = [a.t if not a.host else a.t.to(comm.device) for a in args]
+            recvs = [a.out.reshape(-1) if a.out is not None else
+                     torch.empty(out_numel, dtype=sends[0].dtype, device=comm.device) for a in args]
+        if reduce:
+            _reduce_scatter_device(comm, algo, order, sends, recvs, emu)
+        else:
+            _all_gather_device(comm, algo, sends, recvs, emu)
+        if emu or any(a.host for a in args):
+            torch.cuda.current_stream(comm.device).synchronize()
+            comm.world.check()
+        res = []
+        for a, rv in zip(args, recvs):
+            if a.host:
+                res.append(_finish(a, rv))
+            else:
+                res.append(rv if a.out is None else a.out)
+        return res
+
+    if comm.emulated:
+        return comm._rendezvous(arg, execute)
+    comm.next_base_tag()
+    return execute([arg])[0]
+
+
+# ---------------------------------------------------------------------------
+# public API (reference names)
+# ---------------------------------------------------------------------------
+def ring_all_gather(comm, buf, *, out=None):
+    """Ring all-gather: p-1 neighbour steps (collectives.py:55-76)."""
+    return _run(comm, buf, False, "ring", "ring", out)
+
+
+def recdbl_all_gather(comm, buf, *, out=None):
+    """Recursive-doubling all-gather: log2 p partner steps (collectives.py:107-129)."""
+    return _run(comm, buf, False, "recursive", "ring", out)
+
+
+def direct_all_gather(comm, buf, *, out=None):
+    """One-shot all-gather: every rank pulls every peer's block in one step."""
+    return _run(comm, buf, False, "direct", "ring", out)
+
+
+def ring_reduce_scatter(comm, buf, *, out=None):
+    """Ring reduce-scatter with the add fused into the peer load (collectives.py:79-104)."""
+    return _run(comm, buf, True, "ring", "ring", out)
+
+
+def rechalf_reduce_scatter(comm, buf, *, out=None):
+    """Recursive-halving reduce-scatter, fused add (collectives.py:132-165)."""
+    return _run(comm, buf, True, "recursive", "ring", out)
+
+
+def direct_reduce_scatter(comm, buf, *, order: str = "ring", out=None):
+    """One-shot reduce-scatter: chunk r pulled from every peer and folded in
+    fp32 in ``order`` ("ring" | "recursive" | "rank"), which makes fp32 results
+    bit-identical to the named step-wise algorithm."""
+    if order not in _lib.ORDERS:
+        raise ValueError(f"unknown order {order!r}")
+    return _run(comm, buf, True, "direct", order, out)
+
+
+def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
+    """Dispatching all-gather; ``auto`` picks from the measured selector."""
+    if algorithm == "auto":
+        from .selector import choose_algorithm
+
+        algorithm = choose_algorithm("all_gather", comm.size, _nbytes(buf) * comm.size)
+    if algorithm not in ALL_GATHER_ALGOS:
+        raise Unsupported(f"unknown all-gather algorithm {algorithm!r}")
+    return _run(comm, buf, False, algorithm, "ring", out)
+
+
+def reduce_scatter(comm, buf, *, algorithm: str = "auto", order: str = "ring", out=None):
+    """Dispatching reduce-scatter; ``auto`` picks from the measured selector."""
+    if algorithm == "auto":
+        from .selector import choose_algorithm
+
+        algorithm = choose_algorithm("reduce_scatter", comm.size, _nbytes(buf))
+    if algorithm not in REDUCE_SCATTER_ALGOS:
+        raise Unsupported(f"unknown reduce-scatter algorithm {algorithm!r}")
+    return _run(comm, buf, True, algorithm, order, out)
+
+
+def _nbytes(buf) -> int:
+    if isinstance(buf, torch.Tensor):
+        return buf.numel() * buf.element_size()
+    return as_elements(buf).nbytes
+
+
+def reduce_inplace(acc, other, op: ReduceOp = ReduceOp.SUM):
+    """``acc[i] <- acc[i] + other[i]`` on the GPU (collectives.py:45-52);
+    returns ``acc`` (updated in place for numpy and tensors alike)."""
+    if op is not ReduceOp.SUM:
+        raise ValueError(f"unsupported reduce op {op}")
+    shape_a = tuple(acc.shape)
+    shape_b = tuple(other.shape)
+    if shape_a != shape_b:
+        raise LengthMismatch(f"length mismatch: {shape_a} vs {shape_b}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if isinstance(acc, torch.Tensor) and acc.is_cuda:
+        a = acc
+        b = other if isinstance(other, torch.Tensor) else torch.as_tensor(np.asarray(other))
+        b = b.to(device=a.device, dtype=a.dtype).contiguous()
+    else:
+        a = torch.as_tensor(np.ascontiguousarray(acc)).to(dev)
+        b = torch.as_tensor(np.ascontiguousarray(other, dtype=np.asarray(acc).dtype)).to(dev)
+    if a.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+        raise Unsupported(f"reduce_inplace does not support {a.dtype}")
+    if not a.is_contiguous():
+        raise ValueError("acc must be contiguous")
+    code = _lib.DTYPES[TORCH_DTYPES[a.dtype]]
+    check(lib().pccl_reduce_inplace(a.data_ptr(), b.data_ptr(), a.numel(), code, _stream(a.device)), "reduce_inplace")
+    if isinstance(acc, torch.Tensor) and acc.is_cuda:
+        return acc
+    res = a.cpu().numpy()
+    if isinstance(acc, torch.Tensor):
+        acc.copy_(torch.from_numpy(res))
+    else:
+        np.copyto(acc, res.reshape(acc.shape))
+    return acc

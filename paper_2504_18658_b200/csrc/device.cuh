@@ -1,0 +1,453 @@
+// device.cuh — launch parameters, cross-GPU flag protocol and data-path
+// primitives shared by every collective kernel (sm_100a).
+//
+// Protocol (replaces the tagged P2P transport, collkit/transport/base.py:3-20):
+//   * every rank owns a flag arena (segment 0) mapped into every peer;
+//   * a group (communicator) owns one flag *slot* in every member's arena;
+//   * the WRITER of a signal stores into the READER's arena, the reader polls
+//     its own memory (ld.acquire.sys), the writer publishes with st.release.sys
+//     after a CTA barrier — one NVLink write per signal, no remote polling;
+//   * READY[src][cta] carries a monotonic progress counter
+//     (epoch << 20 | units_done) so flags are never reset between calls: the
+//     per-group epoch plays the role of next_base_tag()'s sequence number
+//     (transport/base.py:131-138);
+//   * DONE[src][cta] = epoch once src has finished reading this rank's buffers
+//     (the WAR guard that lets the caller reuse them after the call);
+//   * META[src][cta] = epoch << 32 | call-signature hash, checked on first
+//     contact: a cross-rank size/dtype/algorithm mismatch raises
+//     LengthMismatch like from_payload (collectives.py:36-42);
+//   * a wait that sees ABORT_BIT, or exceeds the %globaltimer deadline, records
+//     the error in the world's host-mapped error word and floods ABORT into
+//     every member's slot so no CTA on any GPU is left spinning.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#ifndef PCCL_MAXR
+#define PCCL_MAXR 16
+#endif
+#define PCCL_MAX_CTAS 128
+#define PCCL_NSLOTS 256
+#define PCCL_SLOT_WORDS (3 * PCCL_MAXR * PCCL_MAX_CTAS)
+#define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
+#define PCCL_FLAG_BYTES ((size_t)PCCL_NSLOTS * PCCL_SLOT_BYTES)
+#define PCCL_ABORT_BIT (1ull << 63)
+
+namespace pccl {
+
+enum FlagKind { F_READY = 0, F_DONE = 1, F_META = 2 };
+enum Dt { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
+enum Algo { A_DIRECT = 0, A_RING = 1, A_REC = 2 };
+enum Order { O_RING = 0, O_REC = 1, O_RANK = 2 };
+
+// One launch = one or more groups of equal size `gs`; launch row y (blockIdx.y)
+// acts for world rank row_rank[y]. Real mode has a single row; emulation mode
+// has one row per emulated rank. Layout fields are in *units* (a unit is a
+// 16-byte vector when the path is vectorised, else one element / U bytes).
+struct LaunchParams {
+  int gs;           // group size
+  int ctas;         // CTAs per row (== gridDim.x)
+  int nsub;         // pipeline sub-slices per CTA slice
+  int nsubblk;      // sub-blocks per member block / chunk (hierarchical layouts)
+  int local_copy;   // AG: copy own send block into recv
+  int order;        // direct RS fold order
+  int skip_exit;    // 1: no DONE barrier (buffers not reused while peers read)
+  int pad0;
+  int64_t timeout_ns;
+  int64_t blk;              // units per sub-block
+  int64_t sub_stride;       // stride between sub-blocks (shared layout)
+  int64_t istride;          // stride between members' blocks / chunks
+  int64_t send_sub_stride;  // AG: sub-block stride inside send (contiguous: blk)
+  int64_t out_sub_stride;   // RS: sub-block stride inside the final output
+  int64_t base[PCCL_MAXR];  // per row: layout base offset (group-uniform)
+  uint64_t epoch[PCCL_MAXR];
+  uint32_t slot_off[PCCL_MAXR];  // per row: flag slot offset in words
+  uint32_t meta[PCCL_MAXR];      // per row: call-signature hash
+  int8_t row_rank[PCCL_MAXR];
+  int8_t grank[PCCL_MAXR];
+  int8_t gmem[PCCL_MAXR][PCCL_MAXR];  // per row: world ranks of the group
+  uint64_t *flags[PCCL_MAXR];         // per world rank: flag arena
+  char *send[PCCL_MAXR];              // per world rank
+  char *recv[PCCL_MAXR];
+  char *work[PCCL_MAXR];
+  char *out[PCCL_MAXR];
+  volatile int *err;                  // host-mapped error word
+};
+
+// --------------------------------------------------------------------------
+// memory-model primitives
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct Ctx {
+  const LaunchParams *P;
+  int y;   // launch row
+  int r;   // world rank
+  int gi;  // index in group
+  int gs;
+  int b;   // CTA index in row
+  uint64_t epoch;
+  uint64_t *my_slot;
+  uint64_t t0;
+
+  __device__ __forceinline__ int world(int m) const { return P->gmem[y][m]; }
+  __device__ __forceinline__ uint64_t *slot_in(int m) const {
+    return P->flags[world(m)] + P->slot_off[y];
+  }
+  static __device__ __forceinline__ uint64_t *word(uint64_t *slot, int kind, int src, int cta) {
+    return slot + ((size_t)(kind * PCCL_MAXR + src) * PCCL_MAX_CTAS + cta);
+  }
+};
+
+__device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
+  Ctx c;
+  c.P = &P;
+  c.y = blockIdx.y;
+  c.r = P.row_rank[c.y];
+  c.gi = P.grank[c.y];
+  c.gs = P.gs;
+  c.b = blockIdx.x;
+  c.epoch = P.epoch[c.y];
+  c.my_slot = P.flags[c.r] + P.slot_off[c.y];
+  c.t0 = global_timer_ns();
+  return c;
+}
+
+// Flood ABORT into every member's slot (all sources, all CTAs) so that every
+// waiter of this group, on every GPU, wakes up. Called by a whole CTA.
+__device__ __noinline__ void abort_group(const Ctx &c, int code) {
+  if (threadIdx.x == 0 && *c.P->err == 0) {
+    *c.P->err = code;
+    __threadfence_system();
+  }
+  const uint64_t v = PCCL_ABORT_BIT | (uint64_t)code;
+  const int per_member = 2 * PCCL_MAXR * PCCL_MAX_CTAS;  // READY + DONE
+  for (int m = 0; m < c.gs; ++m) {
+    uint64_t *slot = c.slot_in(m);
+    for (int i = threadIdx.x; i < per_member; i += blockDim.x) st_relaxed_sys(slot + i, v);
+  }
+  __threadfence_system();
+}
+
+// Spin (one thread) until word >= target. Returns 0 or an error code.
+__device__ __forceinline__ int spin_ge(const Ctx &c, const uint64_t *w, uint64_t target) {
+  uint32_t it = 0;
+  while (true) {
+    uint64_t v = ld_acquire_sys(w);
+    if (v & PCCL_ABORT_BIT) return (int)(v & 0xff);
+    if (v >= target) return 0;
+    if ((++it & 255u) == 0) {
+      if (*c.P->err != 0) return *c.P->err;
+      if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;  // PCCL_ERR_TIMEOUT
+    }
+  }
+}
+
+// Step-structure helpers shared by the kernels and pccl_schedule (host).
+__host__ __device__ __forceinline__ int ring_prev(int gi, int gs) { return (gi - 1 + gs) % gs; }
+__host__ __device__ __forceinline__ int ring_next(int gi, int gs) { return (gi + 1) % gs; }
+// recursive doubling AG, step k (collectives.py:121-124)
+__host__ __device__ __forceinline__ int recdbl_partner(int gi, int k) { return gi ^ (1 << k); }
+// recursive halving RS, step k (collectives.py:151-153)
+__host__ __device__ __forceinline__ int rechalf_partner(int gi, int gs, int k) { return gi ^ (gs >> (k + 1)); }
+
+__device__ __forceinline__ uint64_t ready_value(uint64_t epoch, int unit) {
+  return (epoch << 20) | (uint64_t)(unit + 1);
+}
+
+// CTA-wide: wait until member m has completed `unit`; optionally verify its
+// call signature. Returns false (after aborting the group) on error.
+__device__ __forceinline__ bool cta_wait(const Ctx &c, int m, int unit, bool check_meta) {
+  int code = 0;
+  if (threadIdx.x == 0) {
+    code = spin_ge(c, Ctx::word(c.my_slot, F_READY, m, c.b), ready_value(c.epoch, unit));
+    if (code == 0 && check_meta) {
+      uint64_t got = ld_acquire_sys(Ctx::word(c.my_slot, F_META, m, c.b));
+      uint64_t want = (c.epoch << 32) | c.P->meta[c.y];
+      if (got != want) code = 4;  // PCCL_ERR_LENGTH_MISMATCH
+    }
+  }
+  int ok = __syncthreads_and(code == 0);
+  if (!ok) {
+    __shared__ int s_code;
+    if (threadIdx.x == 0) s_code = code;
+    __syncthreads();
+    if (s_code != 0) abort_group(c, s_code);
+    return false;
+  }
+  return true;
+}
+
+// CTA-wide: wait for every member in `mask` (bit m) to complete `unit`.
+__device__ __forceinline__ bool cta_wait_mask(const Ctx &c, uint32_t mask, int unit, bool check_meta) {
+  int code = 0;
+  const int m = threadIdx.x;
+  if (m < c.gs && ((mask >> m) & 1u)) {
+    code = spin_ge(c, Ctx::word(c.my_slot, F_READY, m, c.b), ready_value(c.epoch, unit));
+    if (code == 0 && check_meta) {
+      uint64_t got = ld_acquire_sys(Ctx::word(c.my_slot, F_META, m, c.b));
+      if (got != ((c.epoch << 32) | c.P->meta[c.y])) code = 4;
+    }
+  }
+  int ok = __syncthreads_and(code == 0);
+  if (!ok) {
+    __shared__ int s_code;
+    if (threadIdx.x == 0) s_code = 0;
+    __syncthreads();
+    if (code != 0) atomicCAS(&s_code, 0, code);
+    __syncthreads();
+    abort_group(c, s_code ? s_code : 5);
+    return false;
+  }
+  return true;
+}
+
+// CTA-wide: publish completion of `unit` to member m (after a CTA barrier so
+// every thread's stores of the unit are ordered before the release).
+__device__ __forceinline__ void cta_signal(const Ctx &c, int m, int unit) {
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c.epoch, unit));
+}
+__device__ __forceinline__ void cta_signal_mask(const Ctx &c, uint32_t mask, int unit) {
+  __syncthreads();
+  const int m = threadIdx.x;
+  if (m < c.gs && ((mask >> m) & 1u))
+    st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c.epoch, unit));
+}
+// Write this call's signature into every member in mask (ordered before the
+// first READY release to that member by that release).
+__device__ __forceinline__ void cta_publish_meta(const Ctx &c, uint32_t mask) {
+  const int m = threadIdx.x;
+  if (m < c.gs && ((mask >> m) & 1u))
+    st_relaxed_sys(Ctx::word(c.slot_in(m), F_META, c.gi, c.b), (c.epoch << 32) | c.P->meta[c.y]);
+}
+
+// Exit barrier: tell every member in `to` that this CTA has finished reading
+// their buffers; wait until every member in `from` has finished reading ours.
+__device__ __forceinline__ bool cta_exit(const Ctx &c, uint32_t to, uint32_t from) {
+  if (c.P->skip_exit) return true;
+  __syncthreads();
+  const int m = threadIdx.x;
+  if (m < c.gs && ((to >> m) & 1u)) st_release_sys(Ctx::word(c.slot_in(m), F_DONE, c.gi, c.b), c.epoch);
+  int code = 0;
+  if (m < c.gs && ((from >> m) & 1u)) code = spin_ge(c, Ctx::word(c.my_slot, F_DONE, m, c.b), c.epoch);
+  int ok = __syncthreads_and(code == 0);
+  if (!ok) {
+    __shared__ int s_code;
+    if (threadIdx.x == 0) s_code = 0;
+    __syncthreads();
+    if (code != 0) atomicCAS(&s_code, 0, code);
+    __syncthreads();
+    abort_group(c, s_code ? s_code : 5);
+    return false;
+  }
+  return true;
+}
+
+// --------------------------------------------------------------------------
+// slicing: CTA b of C owns [lo,hi) of every sub-block; sub-slice t of nsub
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void split32(int64_t len, int parts, int idx, int64_t &lo, int64_t &hi) {
+  const int64_t n32 = (len + 31) / 32;
+  lo = (n32 * idx / parts) * 32;
+  hi = (n32 * (idx + 1) / parts) * 32;
+  if (lo > len) lo = len;
+  if (hi > len) hi = len;
+}
+__device__ __forceinline__ void cta_subslice(const Ctx &c, int t, int64_t &lo, int64_t &hi) {
+  int64_t a, e;
+  split32(c.P->blk, c.P->ctas, c.b, a, e);
+  int64_t sa, se;
+  split32(e - a, c.P->nsub, t, sa, se);
+  lo = a + sa;
+  hi = a + se;
+}
+
+// --------------------------------------------------------------------------
+// unit types and loads
+// --------------------------------------------------------------------------
+template <int U> struct VecT;
+template <> struct VecT<16> { using T = uint4; };
+template <> struct VecT<8> { using T = uint2; };
+template <> struct VecT<4> { using T = unsigned int; };
+template <> struct VecT<2> { using T = unsigned short; };
+template <> struct VecT<1> { using T = unsigned char; };
+
+// Peer data is read with .cg (L2-coherent, no L1 allocation): it is produced
+// during this kernel by another GPU and published through the flag protocol.
+template <typename T> __device__ __forceinline__ T ld_peer(const T *p) { return __ldcg(p); }
+
+template <int U, int UNROLL>
+__device__ __forceinline__ void copy_units(char *dst, const char *src, int64_t lo, int64_t hi) {
+  using T = typename VecT<U>::T;
+  T *d = reinterpret_cast<T *>(dst);
+  const T *s = reinterpret_cast<const T *>(src);
+  const int nt = blockDim.x;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (int64_t)(UNROLL - 1) * nt < hi; i += (int64_t)UNROLL * nt) {
+    T v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = ld_peer(s + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) d[i + (int64_t)u * nt] = v[u];
+  }
+  for (; i < hi; i += nt) d[i] = ld_peer(s + i);
+}
+
+// --------------------------------------------------------------------------
+// reduction units: VEC -> one uint4 (4 fp32 or 8 bf16/f16), else one element.
+// Accumulation is always fp32 with explicit round-to-nearest adds (no
+// reassociation, no contraction): the fold order is the algorithm's.
+// --------------------------------------------------------------------------
+template <int DT, bool VEC> struct RUnit;
+
+template <> struct RUnit<DT_F32, true> {
+  using T = uint4;
+  static constexpr int N = 4;
+  struct Acc { float v[4]; };
+  static __device__ __forceinline__ Acc load(T u) {
+    Acc a; a.v[0] = __uint_as_float(u.x); a.v[1] = __uint_as_float(u.y);
+    a.v[2] = __uint_as_float(u.z); a.v[3] = __uint_as_float(u.w); return a;
+  }
+  static __device__ __forceinline__ T store(const Acc &a) {
+    return make_uint4(__float_as_uint(a.v[0]), __float_as_uint(a.v[1]), __float_as_uint(a.v[2]),
+                      __float_as_uint(a.v[3]));
+  }
+};
+template <> struct RUnit<DT_F32, false> {
+  using T = unsigned int;
+  static constexpr int N = 1;
+  struct Acc { float v[1]; };
+  static __device__ __forceinline__ Acc load(T u) { Acc a; a.v[0] = __uint_as_float(u); return a; }
+  static __device__ __forceinline__ T store(const Acc &a) { return __float_as_uint(a.v[0]); }
+};
+
+__device__ __forceinline__ float2 bf2_to_f2(unsigned x) {
+  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162 *>(&x);
+  return __bfloat1622float2(h);
+}
+__device__ __forceinline__ unsigned f2_to_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<unsigned *>(&h);
+}
+__device__ __forceinline__ float2 h2_to_f2(unsigned x) {
+  __half2 h = *reinterpret_cast<__half2 *>(&x);
+  return __half22float2(h);
+}
+__device__ __forceinline__ unsigned f2_to_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<unsigned *>(&h);
+}
+
+template <> struct RUnit<DT_BF16, true> {
+  using T = uint4;
+  static constexpr int N = 8;
+  struct Acc { float v[8]; };
+  static __device__ __forceinline__ Acc load(T u) {
+    Acc a; float2 f;
+    f = bf2_to_f2(u.x); a.v[0] = f.x; a.v[1] = f.y;
+    f = bf2_to_f2(u.y); a.v[2] = f.x; a.v[3] = f.y;
+    f = bf2_to_f2(u.z); a.v[4] = f.x; a.v[5] = f.y;
+    f = bf2_to_f2(u.w); a.v[6] = f.x; a.v[7] = f.y;
+    return a;
+  }
+  static __device__ __forceinline__ T store(const Acc &a) {
+    return make_uint4(f2_to_bf2(a.v[0], a.v[1]), f2_to_bf2(a.v[2], a.v[3]), f2_to_bf2(a.v[4], a.v[5]),
+                      f2_to_bf2(a.v[6], a.v[7]));
+  }
+};
+template <> struct RUnit<DT_BF16, false> {
+  using T = unsigned short;
+  static constexpr int N = 1;
+  struct Acc { float v[1]; };
+  static __device__ __forceinline__ Acc load(T u) { Acc a; a.v[0] = __uint_as_float(((unsigned)u) << 16); return a; }
+  static __device__ __forceinline__ T store(const Acc &a) {
+    __nv_bfloat16 h = __float2bfloat16_rn(a.v[0]);
+    return *reinterpret_cast<unsigned short *>(&h);
+  }
+};
+template <> struct RUnit<DT_F16, true> {
+  using T = uint4;
+  static constexpr int N = 8;
+  struct Acc { float v[8]; };
+  static __device__ __forceinline__ Acc load(T u) {
+    Acc a; float2 f;
+    f = h2_to_f2(u.x); a.v[0] = f.x; a.v[1] = f.y;
+    f = h2_to_f2(u.y); a.v[2] = f.x; a.v[3] = f.y;
+    f = h2_to_f2(u.z); a.v[4] = f.x; a.v[5] = f.y;
+    f = h2_to_f2(u.w); a.v[6] = f.x; a.v[7] = f.y;
+    return a;
+  }
+  static __device__ __forceinline__ T store(const Acc &a) {
+    return make_uint4(f2_to_h2(a.v[0], a.v[1]), f2_to_h2(a.v[2], a.v[3]), f2_to_h2(a.v[4], a.v[5]),
+                      f2_to_h2(a.v[6], a.v[7]));
+  }
+};
+template <> struct RUnit<DT_F16, false> {
+  using T = unsigned short;
+  static constexpr int N = 1;
+  struct Acc { float v[1]; };
+  static __device__ __forceinline__ Acc load(T u) {
+    __half h = *reinterpret_cast<__half *>(&u);
+    Acc a; a.v[0] = __half2float(h); return a;
+  }
+  static __device__ __forceinline__ T store(const Acc &a) {
+    __half h = __float2half_rn(a.v[0]);
+    return *reinterpret_cast<unsigned short *>(&h);
+  }
+};
+
+template <typename Acc, int N>
+__device__ __forceinline__ void acc_add(Acc &a, const Acc &b) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) a.v[i] = __fadd_rn(a.v[i], b.v[i]);
+}
+
+// dst[i] = round(a[i] + b[i]) over units [lo,hi); a local, b peer.
+template <int DT, bool VEC, int UNROLL>
+__device__ __forceinline__ void reduce2_units(char *dst, const char *a, const char *b, int64_t lo, int64_t hi) {
+  using R = RUnit<DT, VEC>;
+  using T = typename R::T;
+  T *d = reinterpret_cast<T *>(dst);
+  const T *x = reinterpret_cast<const T *>(a);
+  const T *y = reinterpret_cast<const T *>(b);
+  const int nt = blockDim.x;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (int64_t)(UNROLL - 1) * nt < hi; i += (int64_t)UNROLL * nt) {
+    T vy[UNROLL], vx[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) vy[u] = ld_peer(y + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) vx[u] = __ldcg(x + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      typename R::Acc s = R::load(vx[u]);
+      acc_add<typename R::Acc, R::N>(s, R::load(vy[u]));
+      d[i + (int64_t)u * nt] = R::store(s);
+    }
+  }
+  for (; i < hi; i += nt) {
+    typename R::Acc s = R::load(__ldcg(x + i));
+    acc_add<typename R::Acc, R::N>(s, R::load(ld_peer(y + i)));
+    d[i] = R::store(s);
+  }
+}
+
+}  // namespace pccl

@@ -1,0 +1,304 @@
+// kernels.cuh — the collective kernels (sm_100a). All are pull-based: a rank
+// reads its peers' symmetric buffers over NVLink/NVSwitch with 16-byte .cg
+// loads and writes only its own HBM, so outputs never need to be registered
+// and there is no staging hop. Reductions are fused into the peer-load loop.
+//
+// Step structure (checked against collkit.simnet.build_schedule through
+// pccl_schedule, see step tables in host code):
+//   AG direct     : 1 step, every rank pulls every peer's block.
+//   AG ring       : collectives.py:55-76 — step s pulls block (r-s) from r-1.
+//   AG recursive  : collectives.py:107-129 — step k pulls 2^k blocks from r^2^k.
+//   RS direct     : 1 step, chunk r pulled from every peer, folded in the
+//                   order of the named algorithm (bit-exact fp32).
+//   RS ring       : collectives.py:79-104 — carry chain, one hop per step.
+//   RS recursive  : collectives.py:132-165 — halving butterfly.
+// Each CTA owns a contiguous slice of every block; inside a step the slice is
+// cut into `nsub` sub-slices, and every sub-slice completion is published to
+// the consumer of that step, so step s+1 of sub-slice t overlaps step s of
+// sub-slice t+1 (no per-step bubble).
+#pragma once
+#include "device.cuh"
+
+namespace pccl {
+
+constexpr int kThreads = 512;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ int ilog2(int x) { return 31 - __clz(x); }
+
+// ============================================================================
+// all-gather
+// ============================================================================
+// Member i's block lives at recv + (base + i*istride + t*sub_stride) * U for
+// sub-blocks t < nsubblk; my own contribution is send + t*send_sub_stride*U.
+template <int U>
+__device__ __forceinline__ char *ag_block(const LaunchParams &P, char *buf, int y, int i, int t) {
+  return buf + (P.base[y] + (int64_t)i * P.istride + (int64_t)t * P.sub_stride) * U;
+}
+
+template <int U>
+__device__ __forceinline__ void ag_local_copy(const Ctx &c, int64_t lo, int64_t hi) {
+  const LaunchParams &P = *c.P;
+  for (int t = 0; t < P.nsubblk; ++t)
+    copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U,
+                           lo, hi);
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
+  cta_publish_meta(c, peers);
+  cta_signal_mask(c, peers, 0);  // my send buffer is ready
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  if (P.local_copy) ag_local_copy<U>(c, lo, hi);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  for (int i = 1; i < c.gs; ++i) {
+    const int q = (c.gi + i) % c.gs;  // rotate so every rank reads a different peer
+    const char *src = P.send[c.world(q)];
+    for (int t = 0; t < P.nsubblk; ++t)
+      copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t), src + (int64_t)t * P.send_sub_stride * U, lo, hi);
+  }
+  cta_exit(c, peers, peers);
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub;
+  const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
+  cta_publish_meta(c, 1u << next);
+  // step 0: own block into recv (the block the ring starts forwarding)
+  for (int t = 0; t < nsub; ++t) {
+    int64_t lo, hi;
+    cta_subslice(c, t, lo, hi);
+    if (P.local_copy) ag_local_copy<U>(c, lo, hi);
+    cta_signal(c, next, t);
+  }
+  char *my = P.recv[c.r];
+  const char *pv = P.recv[c.world(prev)];
+  for (int s = 1; s < gs; ++s) {
+    const int blk = (c.gi - s + gs) % gs;  // block received at reference step s-1
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, prev, (s - 1) * nsub + t, s == 1 && t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int j = 0; j < P.nsubblk; ++j)
+        copy_units<U, kUnroll>(ag_block<U>(P, my, c.y, blk, j), ag_block<U>(P, const_cast<char *>(pv), c.y, blk, j), lo,
+                               hi);
+      if (s < gs - 1) cta_signal(c, next, s * nsub + t);
+    }
+  }
+  cta_exit(c, 1u << prev, 1u << next);
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
+  uint32_t partners = 0;
+  for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
+  cta_publish_meta(c, partners);
+  for (int t = 0; t < nsub; ++t) {
+    int64_t lo, hi;
+    cta_subslice(c, t, lo, hi);
+    if (P.local_copy) ag_local_copy<U>(c, lo, hi);
+    cta_signal(c, recdbl_partner(c.gi, 0), t);
+  }
+  char *my = P.recv[c.r];
+  for (int k = 0; k < L; ++k) {
+    const int partner = recdbl_partner(c.gi, k);
+    const char *pr = P.recv[c.world(partner)];
+    const int start = (partner >> k) << k, width = 1 << k;
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, partner, k * nsub + t, t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int i = start; i < start + width; ++i)
+        for (int j = 0; j < P.nsubblk; ++j)
+          copy_units<U, kUnroll>(ag_block<U>(P, my, c.y, i, j), ag_block<U>(P, const_cast<char *>(pr), c.y, i, j), lo,
+                                 hi);
+      if (k + 1 < L) cta_signal(c, recdbl_partner(c.gi, k + 1), (k + 1) * nsub + t);
+    }
+  }
+  cta_exit(c, partners, partners);
+}
+
+// ============================================================================
+// reduce-scatter
+// ============================================================================
+// Chunk c (the part owned by member c) consists of nsubblk sub-blocks at
+// (base + c*istride + t*sub_stride) units in send/work; the final chunk goes to
+// out + t*out_sub_stride units.
+template <typename T>
+__device__ __forceinline__ char *rs_chunk(const LaunchParams &P, char *buf, int y, int c, int t) {
+  return buf + (P.base[y] + (int64_t)c * P.istride + (int64_t)t * P.sub_stride) * (int64_t)sizeof(T);
+}
+
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ LaunchParams P) {
+  using T = typename RUnit<DT, VEC>::T;
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub;
+  const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
+  cta_publish_meta(c, 1u << next);
+  for (int t = 0; t < nsub; ++t) cta_signal(c, next, t);  // my send is ready
+  char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
+  const int pw = c.world(prev);
+  for (int s = 1; s < gs; ++s) {
+    const int ch = ((c.gi - s - 1) % gs + gs) % gs;  // chunk whose carry I extend
+    const bool last = (s == gs - 1);
+    const char *remote = (s == 1) ? P.send[pw] : P.work[pw];
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, prev, (s - 1) * nsub + t, s == 1 && t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int j = 0; j < P.nsubblk; ++j) {
+        char *dst = last ? outp + (int64_t)j * P.out_sub_stride * (int64_t)sizeof(T) : rs_chunk<T>(P, workp, c.y, ch, j);
+        reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, sendp, c.y, ch, j),
+                                        rs_chunk<T>(P, const_cast<char *>(remote), c.y, ch, j), lo, hi);
+      }
+      if (!last) cta_signal(c, next, s * nsub + t);
+    }
+  }
+  cta_exit(c, 1u << prev, 1u << next);
+}
+
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ LaunchParams P) {
+  using T = typename RUnit<DT, VEC>::T;
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
+  uint32_t partners = 0;
+  for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
+  cta_publish_meta(c, partners);
+  for (int t = 0; t < nsub; ++t) cta_signal(c, rechalf_partner(c.gi, gs, 0), t);  // my send is ready
+  char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
+  int lo_c = 0, hi_c = gs;
+  for (int k = 0; k < L; ++k) {
+    const int half = (hi_c - lo_c) / 2, mid = lo_c + half;
+    const int partner = c.gi ^ half;  // == rechalf_partner(c.gi, gs, k)
+    int m0, m1;
+    if (c.gi < mid) { m0 = lo_c; m1 = mid; } else { m0 = mid; m1 = hi_c; }
+    const bool last = (k == L - 1);
+    const int pw = c.world(partner);
+    const char *remote = (k == 0) ? P.send[pw] : P.work[pw];
+    const char *local = (k == 0) ? sendp : workp;
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, partner, k * nsub + t, t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int ch = m0; ch < m1; ++ch)
+        for (int j = 0; j < P.nsubblk; ++j) {
+          char *dst = last ? outp + (int64_t)j * P.out_sub_stride * (int64_t)sizeof(T) : rs_chunk<T>(P, workp, c.y, ch, j);
+          reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, const_cast<char *>(local), c.y, ch, j),
+                                          rs_chunk<T>(P, const_cast<char *>(remote), c.y, ch, j), lo, hi);
+        }
+      if (!last) cta_signal(c, rechalf_partner(c.gi, gs, k + 1), (k + 1) * nsub + t);
+    }
+    lo_c = m0;
+    hi_c = m1;
+  }
+  cta_exit(c, partners, partners);
+}
+
+// Direct reduce-scatter: every member's chunk `gi` is pulled in one step and
+// folded in registers in the named order. Leaves are loaded first (MAXP
+// independent 16-byte loads in flight per thread), then combined with static
+// register indices.
+template <int DT, bool VEC, int ORDER, int MAXP>
+__global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ LaunchParams P) {
+  using R = RUnit<DT, VEC>;
+  using T = typename R::T;
+  using Acc = typename R::Acc;
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, gi = c.gi;
+  const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
+  cta_publish_meta(c, peers);
+  cta_signal_mask(c, peers, 0);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  // source member of leaf position i
+  const T *src[MAXP];
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) {
+    int q;
+    if (ORDER == O_RING) q = (gi + 1 + i) % gs;
+    else if (ORDER == O_REC) q = gi ^ i;
+    else q = i;
+    if (i >= gs) q = gi;
+    src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]);
+  }
+  const int nt = blockDim.x;
+  for (int j = 0; j < P.nsubblk; ++j) {
+    const int64_t off = P.base[c.y] + (int64_t)gi * P.istride + (int64_t)j * P.sub_stride;
+    T *dst = reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
+      T raw[MAXP];
+#pragma unroll
+      for (int i = 0; i < MAXP; ++i) raw[i] = (i < gs) ? ld_peer(src[i] + off + e) : T{};
+      Acc acc;
+      if (ORDER == O_REC) {
+        Acc v[MAXP];
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
+#pragma unroll
+        for (int h = MAXP / 2; h >= 1; h >>= 1) {
+          if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
+#pragma unroll
+            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+          }
+        }
+        acc = v[0];
+      } else if (ORDER == O_RANK) {
+#pragma unroll
+        for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      } else {
+        acc = R::load(raw[0]);
+#pragma unroll
+        for (int i = 1; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      }
+      dst[e] = R::store(acc);
+    }
+  }
+  cta_exit(c, peers, peers);
+}
+
+// ============================================================================
+// device-local helpers
+// ============================================================================
+// Block transpose (hierarchy.py:103-126): out block (a*B + b) = in block (b*A + a)
+// where the input is a B x A grid of blocks. Grid-stride over output units.
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_shuffle(const char *in, char *out, int A, int B, int64_t blk) {
+  using T = typename VecT<U>::T;
+  const T *s = reinterpret_cast<const T *>(in);
+  T *d = reinterpret_cast<T *>(out);
+  const int64_t total = (int64_t)A * B * blk;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ob = o / blk, e = o - ob * blk;
+    const int64_t a = ob / B, b = ob - a * B;
+    d[o] = __ldg(s + (b * A + a) * blk + e);
+  }
+}
+
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_reduce_inplace(char *acc, const char *other, int64_t n) {
+  using R = RUnit<DT, VEC>;
+  using T = typename R::T;
+  T *a = reinterpret_cast<T *>(acc);
+  const T *b = reinterpret_cast<const T *>(other);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    typename R::Acc s = R::load(a[i]);
+    acc_add<typename R::Acc, R::N>(s, R::load(__ldg(b + i)));
+    a[i] = R::store(s);
+  }
+}
+
+}  // namespace pccl

@@ -1,0 +1,1126 @@
+// pccl_b200.cu — C-ABI implementation: worlds (symmetric segments over CUDA
+// IPC), communicators (flag slots + epochs), call planning (staging, layout,
+// vector width, grid) and kernel dispatch. See include/pccl_b200.h.
+#include "../../include/pccl_b200.h"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+using namespace pccl;
+
+namespace {
+
+constexpr int kMaxSegs = 64;
+
+struct Segment {
+  bool used = false;
+  size_t bytes = 0;
+  char *ptr[PCCL_MAXR] = {};      // valid in this process (own, peer-mapped or emulated)
+  bool opened[PCCL_MAXR] = {};    // cudaIpcOpenMemHandle'd (must be closed)
+  bool owned[PCCL_MAXR] = {};     // cudaMalloc'd here (must be freed)
+};
+
+}  // namespace
+
+struct pccl_world {
+  int nranks = 0;
+  int rank = -1;  // -1: emulation
+  int device = 0;
+  bool emu = false;
+  Segment segs[kMaxSegs];
+  int staging = -1;
+  volatile int *err_host = nullptr;
+  int *err_dev = nullptr;
+  uint64_t epoch[PCCL_NSLOTS] = {};
+  std::map<uint32_t, int> slot_of_mask;  // emulation: dynamic slot allocation
+  int sms = 148;
+  int ctas = 0;      // 0: auto
+  int nsub = 4;
+  int threads = kThreads;
+  int64_t timeout_ns = 20ll * 1000 * 1000 * 1000;
+  uint32_t meta_skew[PCCL_MAXR] = {};
+  std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
+};
+
+struct pccl_comm {
+  pccl_world *w = nullptr;
+  int gs = 0;
+  int members[PCCL_MAXR] = {};
+  int gi = -1;  // this process's index (real mode)
+  int slot = 0;
+  int comm_id = 0;
+  uint32_t mask = 0;
+};
+
+namespace {
+
+int cuda_err(cudaError_t e) {
+  if (e == cudaSuccess) return PCCL_SUCCESS;
+  fprintf(stderr, "[pccl_b200] CUDA error: %s\n", cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? PCCL_ERR_OUT_OF_MEMORY : PCCL_ERR_CUDA;
+}
+#define CK(x)                                 \
+  do {                                        \
+    int _s = cuda_err(x);                     \
+    if (_s != PCCL_SUCCESS) return _s;        \
+  } while (0)
+
+size_t dt_size(int dt) {
+  switch (dt) {
+    case PCCL_FLOAT32: return 4;
+    case PCCL_BFLOAT16: return 2;
+    case PCCL_FLOAT16: return 2;
+    case PCCL_UINT8: return 1;
+    case PCCL_INT32: return 4;
+    case PCCL_INT64: return 8;
+    case PCCL_FLOAT64: return 8;
+  }
+  return 0;
+}
+bool is_pow2(int x) { return x >= 1 && (x & (x - 1)) == 0; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+uint32_t hash_meta(int coll, int algo, int order, size_t count, int dtype, int gs) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { h ^= v; h *= 1099511628211ull; };
+  mix(coll); mix(algo); mix(order); mix(count); mix(dtype); mix(gs);
+  return (uint32_t)(h ^ (h >> 32)) & 0x7fffffff;
+}
+
+int slot_for(pccl_world *w, uint32_t mask) {
+  if (!w->emu) return (int)mask;  // real mode: nranks <= 8 -> mask < 256
+  auto it = w->slot_of_mask.find(mask);
+  if (it != w->slot_of_mask.end()) return it->second;
+  int s = (int)w->slot_of_mask.size();
+  if (s >= PCCL_NSLOTS) return -1;
+  w->slot_of_mask[mask] = s;
+  return s;
+}
+
+// Find (segment, offset) of a pointer owned by world rank r.
+bool resolve(pccl_world *w, int r, const void *p, size_t bytes, int *seg, size_t *off) {
+  const char *c = (const char *)p;
+  for (int s = 1; s < kMaxSegs; ++s) {
+    const Segment &S = w->segs[s];
+    if (!S.used || !S.ptr[r]) continue;
+    if (c >= S.ptr[r] && c + bytes <= S.ptr[r] + S.bytes) {
+      *seg = s;
+      *off = (size_t)(c - S.ptr[r]);
+      return true;
+    }
+  }
+  return false;
+}
+
+int max_coresident(const void *kernel, int threads, int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess) return sms;
+  return std::max(1, per_sm) * sms;
+}
+
+// --------------------------------------------------------------------------
+// kernel selection
+// --------------------------------------------------------------------------
+using KernelFn = void (*)(LaunchParams);
+
+KernelFn ag_kernel(int algo, int U) {
+#define AGK(A, K)                              \
+  if (algo == A) {                             \
+    switch (U) {                               \
+      case 16: return (KernelFn)K<16>;         \
+      case 8: return (KernelFn)K<8>;           \
+      case 4: return (KernelFn)K<4>;           \
+      case 2: return (KernelFn)K<2>;           \
+      default: return (KernelFn)K<1>;          \
+    }                                          \
+  }
+  AGK(A_DIRECT, k_ag_direct)
+  AGK(A_RING, k_ag_ring)
+  AGK(A_REC, k_ag_rec)
+#undef AGK
+  return nullptr;
+}
+
+template <int DT, bool VEC>
+KernelFn rs_kernel_dt(int algo, int order, int maxp) {
+  if (algo == A_RING) return (KernelFn)k_rs_ring<DT, VEC>;
+  if (algo == A_REC) return (KernelFn)k_rs_rec<DT, VEC>;
+#define RSD(O)                                                   \
+  if (order == O) {                                              \
+    if (!VEC) return (KernelFn)k_rs_direct<DT, VEC, O, 16>;      \
+    switch (maxp) {                                              \
+      case 2: return (KernelFn)k_rs_direct<DT, VEC, O, 2>;       \
+      case 4: return (KernelFn)k_rs_direct<DT, VEC, O, 4>;       \
+      case 8: return (KernelFn)k_rs_direct<DT, VEC, O, 8>;       \
+      default: return (KernelFn)k_rs_direct<DT, VEC, O, 16>;     \
+    }                                                            \
+  }
+  RSD(O_RING)
+  RSD(O_REC)
+  RSD(O_RANK)
+#undef RSD
+  return nullptr;
+}
+
+KernelFn rs_kernel(int dt, bool vec, int algo, int order, int maxp) {
+  if (dt == PCCL_FLOAT32) return vec ? rs_kernel_dt<DT_F32, true>(algo, order, maxp) : rs_kernel_dt<DT_F32, false>(algo, order, maxp);
+  if (dt == PCCL_BFLOAT16) return vec ? rs_kernel_dt<DT_BF16, true>(algo, order, maxp) : rs_kernel_dt<DT_BF16, false>(algo, order, maxp);
+  if (dt == PCCL_FLOAT16) return vec ? rs_kernel_dt<DT_F16, true>(algo, order, maxp) : rs_kernel_dt<DT_F16, false>(algo, order, maxp);
+  return nullptr;
+}
+
+// --------------------------------------------------------------------------
+// a planned launch: rows (world ranks acted for) and their groups
+// --------------------------------------------------------------------------
+struct Row {
+  int rank;              // world rank
+  const pccl_comm *g;    // its group
+};
+
+struct Plan {
+  int coll;  // 0 AG, 1 RS
+  int algo;
+  int order = 0;
+  int dtype;
+  size_t count;          // AG: elements per member block; RS: elements per chunk
+  int gs;
+  std::vector<Row> rows;
+  // layout in ELEMENTS (converted to units at launch)
+  int nsubblk = 1;
+  int64_t blk = 0, sub_stride = 0, istride = 0, send_sub_stride = 0, out_sub_stride = 0;
+  int64_t base[PCCL_MAXR] = {};  // by world rank
+  int local_copy = 1;
+  // per world rank buffers
+  char *send[PCCL_MAXR] = {}, *recv[PCCL_MAXR] = {}, *work[PCCL_MAXR] = {}, *out[PCCL_MAXR] = {};
+  uint32_t place = 0;  // symmetric-placement hash (real mode)
+};
+
+int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
+  const size_t es = dt_size(pl.dtype);
+  LaunchParams P;
+  memset(&P, 0, sizeof(P));
+  P.gs = pl.gs;
+  P.nsubblk = pl.nsubblk;
+  P.local_copy = pl.local_copy;
+  P.order = pl.order;
+  P.timeout_ns = w->timeout_ns;
+  P.err = w->err_dev;
+  P.nsub = std::max(1, std::min(w->nsub, 64));
+
+  // ---- unit size: largest power of two dividing every byte offset/pointer
+  const int64_t bytes_terms[] = {pl.blk * (int64_t)es, pl.sub_stride * (int64_t)es, pl.istride * (int64_t)es,
+                                 pl.send_sub_stride * (int64_t)es, pl.out_sub_stride * (int64_t)es};
+  uint64_t acc = 0;
+  for (int64_t t : bytes_terms) acc |= (uint64_t)t;
+  for (const Row &rw : pl.rows) {
+    acc |= (uint64_t)(pl.base[rw.rank] * (int64_t)es);
+    for (int m = 0; m < rw.g->gs; ++m) {
+      const int q = rw.g->members[m];
+      for (char *p : {pl.send[q], pl.recv[q], pl.work[q], pl.out[q]}) acc |= (uint64_t)(uintptr_t)p;
+    }
+  }
+  int U;  // bytes per unit
+  KernelFn k;
+  if (pl.coll == PCCL_ALL_GATHER) {
+    U = 16;
+    while (U > 1 && (acc & (uint64_t)(U - 1))) U >>= 1;
+    if ((size_t)U < es && es <= 16 && !(acc & (es - 1))) U = (int)es;
+    k = ag_kernel(pl.algo, U);
+  } else {
+    const bool vec = (acc & 15ull) == 0;
+    U = vec ? 16 : (int)es;
+    int maxp = 2;
+    while (maxp < pl.gs) maxp <<= 1;
+    k = rs_kernel(pl.dtype, vec, pl.algo, pl.order, maxp);
+  }
+  if (!k) return PCCL_ERR_UNSUPPORTED;
+  const int64_t epu = U / (int64_t)es > 0 ? U / (int64_t)es : 1;  // elements per unit
+  auto units = [&](int64_t e) { return (pl.coll == PCCL_ALL_GATHER) ? e * (int64_t)es / U : e / epu; };
+  P.blk = units(pl.blk);
+  P.sub_stride = units(pl.sub_stride);
+  P.istride = units(pl.istride);
+  P.send_sub_stride = units(pl.send_sub_stride);
+  P.out_sub_stride = units(pl.out_sub_stride);
+
+  // ---- rows
+  const int nrows = (int)pl.rows.size();
+  std::map<int, uint64_t> slot_epoch;  // bump each group's epoch once per launch
+  for (int y = 0; y < nrows; ++y) {
+    const Row &rw = pl.rows[y];
+    const pccl_comm *g = rw.g;
+    P.row_rank[y] = (int8_t)rw.rank;
+    int gi = -1;
+    for (int m = 0; m < g->gs; ++m) {
+      P.gmem[y][m] = (int8_t)g->members[m];
+      if (g->members[m] == rw.rank) gi = m;
+    }
+    P.grank[y] = (int8_t)gi;
+    P.base[y] = units(pl.base[rw.rank]);
+    P.slot_off[y] = (uint32_t)((size_t)g->slot * PCCL_SLOT_WORDS);
+    auto it = slot_epoch.find(g->slot);
+    if (it == slot_epoch.end()) it = slot_epoch.emplace(g->slot, ++w->epoch[g->slot]).first;
+    P.epoch[y] = it->second;
+    P.meta[y] = (hash_meta(pl.coll, pl.algo, pl.order, pl.count, pl.dtype, pl.gs) ^ (pl.place * 2654435761u) ^
+                 w->meta_skew[rw.rank]) & 0x7fffffffu;
+  }
+  for (int q = 0; q < w->nranks; ++q) {
+    P.flags[q] = (uint64_t *)w->segs[0].ptr[q];
+    P.send[q] = pl.send[q];
+    P.recv[q] = pl.recv[q];
+    P.work[q] = pl.work[q];
+    P.out[q] = pl.out[q];
+  }
+
+  // ---- grid
+  const int threads = kThreads;
+  int ctas = w->ctas > 0 ? w->ctas : (w->emu ? 16 : 32);
+  ctas = std::min(ctas, PCCL_MAX_CTAS);
+  if (w->emu) {
+    const int cap = max_coresident((const void *)k, threads, w->sms);
+    ctas = std::max(1, std::min(ctas, cap / nrows));
+  }
+  P.ctas = ctas;
+  dim3 grid(ctas, nrows), block(threads);
+  if (w->emu) {
+    void *args[] = {&P};
+    CK(cudaLaunchCooperativeKernel((const void *)k, grid, block, args, 0, stream));
+  } else {
+    k<<<grid, block, 0, stream>>>(P);
+    CK(cudaGetLastError());
+  }
+  return PCCL_SUCCESS;
+}
+
+// Per-rank buffer binding with staging ------------------------------------
+// A buffer peers must read is "symmetric": either it lies in a registered
+// segment (then every rank must pass the same segment offset — checked on the
+// device through the call signature) or it is copied into the staging
+// segment at an SPMD-uniform offset.
+struct Binder {
+  pccl_world *w;
+  cudaStream_t stream;
+  size_t cursor = 0;  // staging bump pointer (bytes), SPMD-uniform
+  int status = PCCL_SUCCESS;
+  uint32_t place = 0;  // hash of symmetric placements (real mode)
+
+  char *stage(int r, size_t bytes, size_t *off_out) {
+    size_t off = cursor;
+    cursor += align256(bytes);
+    if (w->staging < 0 || cursor > w->segs[w->staging].bytes) {
+      status = PCCL_ERR_OUT_OF_MEMORY;
+      return nullptr;
+    }
+    *off_out = off;
+    return w->segs[w->staging].ptr[r] + off;
+  }
+  void fill(int r, int seg, size_t off, char *const *dst_unused, char **per, char *own) {
+    (void)dst_unused;
+    for (int q = 0; q < w->nranks; ++q) {
+      if (w->emu && q != r) continue;  // emulation: each row binds its own rank only
+      per[q] = w->segs[seg].ptr[q] ? w->segs[seg].ptr[q] + off : nullptr;
+    }
+    per[r] = own;
+  }
+  // Returns false on error. *staged = local staging alias when copied.
+  bool symmetric(int r, const void *user, size_t bytes, bool copy_in, char **per, char **staged) {
+    int seg;
+    size_t off;
+    if (staged) *staged = nullptr;
+    if (bytes == 0) {
+      per[r] = (char *)user;
+      return true;
+    }
+    if (resolve(w, r, user, bytes, &seg, &off)) {
+      fill(r, seg, off, nullptr, per, (char *)user);
+      place = place * 31u + (uint32_t)seg * 7919u + (uint32_t)(off >> 8) + 1u;
+      return true;
+    }
+    size_t soff;
+    char *p = stage(r, bytes, &soff);
+    if (!p) return false;
+    fill(r, w->staging, soff, nullptr, per, p);
+    place = place * 31u + 17u;
+    if (copy_in && cudaMemcpyAsync(p, user, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) {
+      status = PCCL_ERR_CUDA;
+      return false;
+    }
+    if (staged) *staged = p;
+    return true;
+  }
+  // Internal symmetric scratch (same staging offset on every rank).
+  bool scratch(int r, size_t bytes, char **per) {
+    size_t soff;
+    char *p = stage(r, bytes, &soff);
+    if (!p) return false;
+    fill(r, w->staging, soff, nullptr, per, p);
+    return true;
+  }
+};
+
+int check_world_err(pccl_world *w) {
+  int e = *w->err_host;
+  if (e) {
+    *w->err_host = 0;
+    return e;
+  }
+  return PCCL_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// flat collectives (shared by real and emulation mode)
+// --------------------------------------------------------------------------
+// ranks: world ranks this process executes (real: {me}; emulation: all members)
+int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const void *const *sends,
+                  void *const *recvs, size_t count, int dtype, cudaStream_t stream) {
+  pccl_world *w = c->w;
+  const size_t es = dt_size(dtype);
+  if (!es) return PCCL_ERR_INVALID_ARGUMENT;
+  if (algo < 0 || algo > 2) return PCCL_ERR_INVALID_ARGUMENT;
+  if (algo == A_REC && !is_pow2(c->gs)) return PCCL_ERR_NON_POWER_OF_TWO;
+  CK(cudaSetDevice(w->device));
+  const int gs = c->gs;
+  const size_t blk_bytes = count * es;
+  if (gs == 1) {  // collectives.py:66-67
+    for (size_t i = 0; i < ranks.size(); ++i)
+      if (blk_bytes && sends[i] != recvs[i])
+        CK(cudaMemcpyAsync(recvs[i], sends[i], blk_bytes, cudaMemcpyDeviceToDevice, stream));
+    return PCCL_SUCCESS;
+  }
+  Plan pl;
+  pl.coll = PCCL_ALL_GATHER;
+  pl.algo = algo;
+  pl.dtype = dtype;
+  pl.count = count;
+  pl.gs = gs;
+  pl.blk = (int64_t)count;
+  pl.istride = (int64_t)count;
+  pl.send_sub_stride = (int64_t)count;
+  Binder B{w, stream};
+  std::vector<std::pair<char *, char *>> copy_out;  // (staged recv, user recv)
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    int gi = -1;
+    for (int m = 0; m < gs; ++m)
+      if (c->members[m] == r) gi = m;
+    if (gi < 0) return PCCL_ERR_INDEX_OUT_OF_RANGE;
+    pl.rows.push_back({r, c});
+    B.cursor = 0;
+    if (algo == A_DIRECT) {
+      // peers read my send; my recv is written locally only
+      if (!B.symmetric(r, sends[i], blk_bytes, true, pl.send, nullptr)) return B.status;
+      pl.recv[r] = (char *)recvs[i];
+      pl.local_copy = sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+    } else {
+      // peers forward out of my recv; send is read locally only
+      char *staged = nullptr;
+      if (!B.symmetric(r, recvs[i], gs * blk_bytes, false, pl.recv, &staged)) return B.status;
+      if (staged) copy_out.push_back({staged, (char *)recvs[i]});
+      pl.send[r] = (char *)sends[i];
+      pl.local_copy = staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+    }
+  }
+  pl.place = w->emu ? 0 : B.place;
+  int s = launch(w, pl, stream);
+  if (s) return s;
+  for (auto &co : copy_out) CK(cudaMemcpyAsync(co.second, co.first, gs * blk_bytes, cudaMemcpyDeviceToDevice, stream));
+  return PCCL_SUCCESS;
+}
+
+int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> &ranks, const void *const *sends,
+                      void *const *recvs, size_t recvcount, int dtype, cudaStream_t stream) {
+  pccl_world *w = c->w;
+  if (dtype != PCCL_FLOAT32 && dtype != PCCL_BFLOAT16 && dtype != PCCL_FLOAT16) return PCCL_ERR_UNSUPPORTED;
+  if (algo < 0 || algo > 2 || order < 0 || order > 2) return PCCL_ERR_INVALID_ARGUMENT;
+  const int gs = c->gs;
+  if (algo == A_REC && !is_pow2(gs)) return PCCL_ERR_NON_POWER_OF_TWO;
+  if (algo == A_DIRECT && order == O_REC && !is_pow2(gs)) return PCCL_ERR_NON_POWER_OF_TWO;
+  CK(cudaSetDevice(w->device));
+  const size_t es = dt_size(dtype);
+  const size_t chunk_bytes = recvcount * es;
+  if (gs == 1) {  // collectives.py:88-89
+    for (size_t i = 0; i < ranks.size(); ++i)
+      if (chunk_bytes && sends[i] != recvs[i])
+        CK(cudaMemcpyAsync(recvs[i], sends[i], chunk_bytes, cudaMemcpyDeviceToDevice, stream));
+    return PCCL_SUCCESS;
+  }
+  Plan pl;
+  pl.coll = PCCL_REDUCE_SCATTER;
+  pl.algo = algo;
+  pl.order = algo == A_DIRECT ? order : 0;
+  pl.dtype = dtype;
+  pl.count = recvcount;
+  pl.gs = gs;
+  pl.blk = (int64_t)recvcount;
+  pl.istride = (int64_t)recvcount;
+  pl.out_sub_stride = (int64_t)recvcount;
+  Binder B{w, stream};
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    bool member = false;
+    for (int m = 0; m < gs; ++m) member |= c->members[m] == r;
+    if (!member) return PCCL_ERR_INDEX_OUT_OF_RANGE;
+    pl.rows.push_back({r, c});
+    B.cursor = 0;
+    if (!B.symmetric(r, sends[i], gs * chunk_bytes, true, pl.send, nullptr)) return B.status;
+    if (algo != A_DIRECT) {
+      B.cursor = align256(gs * chunk_bytes);  // work at the same offset on every rank
+      if (!B.scratch(r, gs * chunk_bytes, pl.work)) return B.status;
+    }
+    pl.out[r] = (char *)recvs[i];
+  }
+  pl.place = w->emu ? 0 : B.place;
+  return launch(w, pl, stream);
+}
+
+std::vector<int> one(int r) { return std::vector<int>{r}; }
+
+pccl_comm *cached_group(pccl_world *w, const std::vector<int> &members, int comm_id) {
+  uint32_t mask = 0;
+  for (int m : members) mask |= 1u << m;
+  // key also on order: same set, different order would need its own object
+  uint32_t key = mask;
+  auto it = w->comm_cache.find(key);
+  if (it != w->comm_cache.end()) {
+    bool same = it->second->gs == (int)members.size();
+    for (size_t i = 0; same && i < members.size(); ++i) same = it->second->members[i] == members[i];
+    if (same) return it->second;
+  }
+  pccl_comm *c = nullptr;
+  if (pccl_comm_create(w, members.data(), (int)members.size(), comm_id, &c) != PCCL_SUCCESS) return nullptr;
+  if (it != w->comm_cache.end()) pccl_comm_destroy(it->second);
+  w->comm_cache[key] = c;
+  return c;
+}
+
+// --------------------------------------------------------------------------
+// hierarchical (hierarchy.py:158-195); virtual nodes n = g / M, local j = g % M
+// --------------------------------------------------------------------------
+int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector<int> &ranks,
+                       const void *const *sends, void *const *recvs, size_t count, int dtype, cudaStream_t stream) {
+  if (N < 1 || M < 1 || N * M != w->nranks) return PCCL_ERR_LENGTH_MISMATCH;
+  if (inter != A_RING && inter != A_REC) return PCCL_ERR_INVALID_ARGUMENT;
+  if (inter == A_REC && !is_pow2(N)) return PCCL_ERR_NON_POWER_OF_TWO;
+  const size_t es = dt_size(dtype);
+  if (!es) return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  const int p = N * M;
+  const size_t out_bytes = (size_t)p * count * es;
+  // symmetric output (both phases forward out of it)
+  Binder B{w, stream};
+  char *outp[PCCL_MAXR] = {};
+  std::vector<std::pair<char *, char *>> copy_out;
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    B.cursor = 0;
+    char *staged = nullptr;
+    if (!B.symmetric(r, recvs[i], out_bytes, false, outp, &staged)) return B.status;
+    if (staged) copy_out.push_back({staged, (char *)recvs[i]});
+  }
+  const uint32_t place = w->emu ? 0 : B.place;
+  // phase 1: inter-node all-gather on every stride-M group, blocks land at
+  // their global positions (g*count) directly (fused shuffle)
+  if (N > 1) {
+    Plan pl;
+    pl.coll = PCCL_ALL_GATHER; pl.algo = inter; pl.dtype = dtype; pl.count = count; pl.gs = N;
+    pl.blk = (int64_t)count; pl.istride = (int64_t)M * count; pl.send_sub_stride = (int64_t)count;
+    pl.local_copy = 1;
+    pl.place = place;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i], j = r % M;
+      std::vector<int> mem;
+      for (int n = 0; n < N; ++n) mem.push_back(n * M + j);
+      pccl_comm *g = cached_group(w, mem, 1 + j);
+      if (!g) return PCCL_ERR_CUDA;
+      pl.rows.push_back({r, g});
+      pl.base[r] = (int64_t)j * count;
+      pl.send[r] = (char *)sends[i];
+    }
+    for (int q = 0; q < w->nranks; ++q) { pl.recv[q] = outp[q]; pl.base[q] = (int64_t)(q % M) * count; }
+    int s = launch(w, pl, stream);
+    if (s) return s;
+  } else {
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i];
+      if (count) CK(cudaMemcpyAsync(outp[r] + (size_t)r * count * es, sends[i], count * es, cudaMemcpyDeviceToDevice, stream));
+    }
+  }
+  // phase 2: intra-node ring all-gather; member l's block = N sub-blocks at
+  // (n*M + l)*count
+  if (M > 1) {
+    Plan pl;
+    pl.coll = PCCL_ALL_GATHER; pl.algo = A_RING; pl.dtype = dtype; pl.count = (size_t)N * count; pl.gs = M;
+    pl.nsubblk = N; pl.blk = (int64_t)count; pl.sub_stride = (int64_t)M * count; pl.istride = (int64_t)count;
+    pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i], n = r / M;
+      std::vector<int> mem;
+      for (int l = 0; l < M; ++l) mem.push_back(n * M + l);
+      pccl_comm *g = cached_group(w, mem, 1 + M + n);
+      if (!g) return PCCL_ERR_CUDA;
+      pl.rows.push_back({r, g});
+    }
+    for (int q = 0; q < w->nranks; ++q) { pl.recv[q] = outp[q]; pl.send[q] = outp[q]; }
+    int s = launch(w, pl, stream);
+    if (s) return s;
+  }
+  for (auto &co : copy_out) CK(cudaMemcpyAsync(co.second, co.first, out_bytes, cudaMemcpyDeviceToDevice, stream));
+  return PCCL_SUCCESS;
+}
+
+int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::vector<int> &ranks,
+                           const void *const *sends, void *const *recvs, size_t n, int dtype, cudaStream_t stream) {
+  if (N < 1 || M < 1 || N * M != w->nranks) return PCCL_ERR_LENGTH_MISMATCH;
+  if (inter != A_RING && inter != A_REC) return PCCL_ERR_INVALID_ARGUMENT;
+  if (inter == A_REC && !is_pow2(N)) return PCCL_ERR_NON_POWER_OF_TWO;
+  if (dtype != PCCL_FLOAT32 && dtype != PCCL_BFLOAT16 && dtype != PCCL_FLOAT16) return PCCL_ERR_UNSUPPORTED;
+  CK(cudaSetDevice(w->device));
+  const size_t es = dt_size(dtype);
+  const int p = N * M;
+  const size_t in_bytes = (size_t)p * n * es, part_bytes = (size_t)N * n * es;
+  Binder B{w, stream};
+  char *sendp[PCCL_MAXR] = {}, *work[PCCL_MAXR] = {}, *part[PCCL_MAXR] = {}, *work2[PCCL_MAXR] = {};
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    B.cursor = 0;
+    if (!B.symmetric(r, sends[i], in_bytes, true, sendp, nullptr)) return B.status;
+    B.cursor = align256(in_bytes);
+    if (!B.scratch(r, in_bytes, work) || !B.scratch(r, part_bytes, part) || !B.scratch(r, part_bytes, work2))
+      return B.status;
+  }
+  const uint32_t place = w->emu ? 0 : B.place;
+  // phase 1: intra ring reduce-scatter; chunk l = N sub-blocks {nd*M + l}
+  if (M > 1) {
+    Plan pl;
+    pl.coll = PCCL_REDUCE_SCATTER; pl.algo = A_RING; pl.dtype = dtype; pl.count = (size_t)N * n; pl.gs = M;
+    pl.nsubblk = N; pl.blk = (int64_t)n; pl.sub_stride = (int64_t)M * n; pl.istride = (int64_t)n;
+    pl.out_sub_stride = (int64_t)n; pl.place = place;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i], nd = r / M;
+      std::vector<int> mem;
+      for (int l = 0; l < M; ++l) mem.push_back(nd * M + l);
+      pccl_comm *g = cached_group(w, mem, 1 + M + nd);
+      if (!g) return PCCL_ERR_CUDA;
+      pl.rows.push_back({r, g});
+    }
+    for (int q = 0; q < w->nranks; ++q) { pl.send[q] = sendp[q]; pl.work[q] = work[q]; pl.out[q] = part[q]; }
+    int s = launch(w, pl, stream);
+    if (s) return s;
+  } else {
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i];
+      if (part_bytes) CK(cudaMemcpyAsync(part[r], sendp[r], part_bytes, cudaMemcpyDeviceToDevice, stream));
+    }
+  }
+  // phase 2: inter reduce-scatter (ring or halving) over the node partials
+  if (N > 1) {
+    Plan pl;
+    pl.coll = PCCL_REDUCE_SCATTER; pl.algo = inter; pl.dtype = dtype; pl.count = n; pl.gs = N;
+    pl.blk = (int64_t)n; pl.istride = (int64_t)n; pl.out_sub_stride = (int64_t)n; pl.place = place;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i], j = r % M;
+      std::vector<int> mem;
+      for (int nd = 0; nd < N; ++nd) mem.push_back(nd * M + j);
+      pccl_comm *g = cached_group(w, mem, 1 + j);
+      if (!g) return PCCL_ERR_CUDA;
+      pl.rows.push_back({r, g});
+      pl.out[r] = (char *)recvs[i];
+    }
+    for (int q = 0; q < w->nranks; ++q) { pl.send[q] = part[q]; pl.work[q] = work2[q]; }
+    return launch(w, pl, stream);
+  }
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r = ranks[i];
+    if (n) CK(cudaMemcpyAsync(recvs[i], part[r], n * es, cudaMemcpyDeviceToDevice, stream));
+  }
+  return PCCL_SUCCESS;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char *pccl_error_string(int s) {
+  switch (s) {
+    case PCCL_SUCCESS: return "success";
+    case PCCL_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case PCCL_ERR_NON_POWER_OF_TWO: return "algorithm requires a power-of-two group size";
+    case PCCL_ERR_NOT_DIVISIBLE: return "buffer not divisible into equal chunks";
+    case PCCL_ERR_LENGTH_MISMATCH: return "buffer lengths disagree across ranks";
+    case PCCL_ERR_TIMEOUT: return "peer did not arrive before the deadline";
+    case PCCL_ERR_PEER_UNREACHABLE: return "peer unreachable";
+    case PCCL_ERR_UNSUPPORTED: return "unsupported collective/algorithm/dtype";
+    case PCCL_ERR_INVALID_TOPOLOGY: return "invalid topology";
+    case PCCL_ERR_INDEX_OUT_OF_RANGE: return "rank out of range";
+    case PCCL_ERR_CUDA: return "CUDA runtime error";
+    case PCCL_ERR_OUT_OF_MEMORY: return "staging segment too small";
+  }
+  return "unknown status";
+}
+
+int pccl_version(void) { return 100; }
+
+static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu) {
+  w->nranks = nranks;
+  w->rank = rank;
+  w->device = device;
+  w->emu = emu;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  w->sms = prop.multiProcessorCount;
+  void *h = nullptr;
+  CK(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
+  memset(h, 0, 64);
+  w->err_host = (volatile int *)h;
+  CK(cudaHostGetDevicePointer((void **)&w->err_dev, h, 0));
+  if (const char *t = getenv("PCCL_TIMEOUT_MS")) w->timeout_ns = atoll(t) * 1000000ll;
+  if (const char *t = getenv("PCCL_CTAS")) w->ctas = atoi(t);
+  if (const char *t = getenv("PCCL_NSUB")) w->nsub = atoi(t);
+  int seg = -1;
+  int s = pccl_segment_create(w, PCCL_FLAG_BYTES, &seg);
+  if (s) return s;
+  for (int q = 0; q < nranks; ++q)
+    if (w->segs[0].ptr[q]) CK(cudaMemset(w->segs[0].ptr[q], 0, PCCL_FLAG_BYTES));
+  CK(cudaDeviceSynchronize());
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_create(int nranks, int rank, int device, pccl_world_t *out) {
+  if (!out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return PCCL_ERR_INVALID_ARGUMENT;
+  pccl_world *w = new pccl_world();
+  int s = world_init(w, nranks, rank, device, false);
+  if (s) { delete w; return s; }
+  *out = w;
+  return PCCL_SUCCESS;
+}
+
+int pccl_emu_world_create(int nranks, int device, pccl_world_t *out) {
+  if (!out || nranks < 1 || nranks > PCCL_MAXR) return PCCL_ERR_INVALID_ARGUMENT;
+  pccl_world *w = new pccl_world();
+  int s = world_init(w, nranks, -1, device, true);
+  if (s) { delete w; return s; }
+  *out = w;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_destroy(pccl_world_t w) {
+  if (!w) return PCCL_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(w->device);
+  cudaDeviceSynchronize();
+  for (auto &kv : w->comm_cache) delete kv.second;
+  for (int s = kMaxSegs - 1; s >= 0; --s)
+    if (w->segs[s].used) pccl_segment_destroy(w, s);
+  if (w->err_host) cudaFreeHost((void *)w->err_host);
+  delete w;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_check(pccl_world_t w) {
+  if (!w) return PCCL_ERR_INVALID_ARGUMENT;
+  return check_world_err(w);
+}
+
+int pccl_world_reset_flags(pccl_world_t w) {
+  if (!w) return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  CK(cudaDeviceSynchronize());
+  for (int q = 0; q < w->nranks; ++q)
+    if (w->segs[0].ptr[q] && w->segs[0].owned[q]) CK(cudaMemset(w->segs[0].ptr[q], 0, PCCL_FLAG_BYTES));
+  CK(cudaDeviceSynchronize());
+  memset(w->epoch, 0, sizeof(w->epoch));
+  *w->err_host = 0;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads) {
+  if (!w || ctas < 0 || ctas > PCCL_MAX_CTAS || nsub < 0 || nsub > 64) return PCCL_ERR_INVALID_ARGUMENT;
+  w->ctas = ctas;
+  if (nsub) w->nsub = nsub;
+  (void)threads;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms) {
+  if (!w || ms <= 0) return PCCL_ERR_INVALID_ARGUMENT;
+  w->timeout_ns = ms * 1000000ll;
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id) {
+  if (!w || !seg_id) return PCCL_ERR_INVALID_ARGUMENT;
+  int s = -1;
+  for (int i = 0; i < kMaxSegs; ++i)
+    if (!w->segs[i].used) { s = i; break; }
+  if (s < 0) return PCCL_ERR_OUT_OF_MEMORY;
+  CK(cudaSetDevice(w->device));
+  Segment &S = w->segs[s];
+  S = Segment();
+  S.bytes = bytes;
+  const size_t alloc = std::max<size_t>(bytes, 256);
+  if (w->emu) {
+    for (int q = 0; q < w->nranks; ++q) {
+      CK(cudaMalloc((void **)&S.ptr[q], alloc));
+      S.owned[q] = true;
+    }
+  } else {
+    CK(cudaMalloc((void **)&S.ptr[w->rank], alloc));
+    S.owned[w->rank] = true;
+  }
+  S.used = true;
+  *seg_id = s;
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_export(pccl_world_t w, int seg_id, void *handle_out) {
+  if (!w || w->emu || seg_id < 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || !handle_out)
+    return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, w->segs[seg_id].ptr[w->rank]));
+  memcpy(handle_out, &h, sizeof(h));
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_import(pccl_world_t w, int seg_id, const void *handles) {
+  if (!w || w->emu || seg_id < 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || !handles)
+    return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  Segment &S = w->segs[seg_id];
+  for (int q = 0; q < w->nranks; ++q) {
+    if (q == w->rank || S.ptr[q]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char *)handles + (size_t)q * PCCL_IPC_HANDLE_BYTES, sizeof(h));
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[pccl_b200] rank %d cannot map segment %d of rank %d: %s\n", w->rank, seg_id, q,
+              cudaGetErrorString(e));
+      return PCCL_ERR_PEER_UNREACHABLE;
+    }
+    S.ptr[q] = (char *)p;
+    S.opened[q] = true;
+  }
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_ptr(pccl_world_t w, int seg_id, int rank, void **ptr, size_t *bytes) {
+  if (!w || seg_id < 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || rank < 0 || rank >= w->nranks)
+    return PCCL_ERR_INVALID_ARGUMENT;
+  if (ptr) *ptr = w->segs[seg_id].ptr[rank];
+  if (bytes) *bytes = w->segs[seg_id].bytes;
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_destroy(pccl_world_t w, int seg_id) {
+  if (!w || seg_id < 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used) return PCCL_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(w->device);
+  cudaDeviceSynchronize();
+  Segment &S = w->segs[seg_id];
+  for (int q = 0; q < w->nranks; ++q) {
+    if (S.opened[q]) cudaIpcCloseMemHandle(S.ptr[q]);
+    if (S.owned[q]) cudaFree(S.ptr[q]);
+  }
+  S = Segment();
+  if (w->staging == seg_id) w->staging = -1;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_set_staging(pccl_world_t w, int seg_id) {
+  if (!w || seg_id <= 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used) return PCCL_ERR_INVALID_ARGUMENT;
+  w->staging = seg_id;
+  return PCCL_SUCCESS;
+}
+
+size_t pccl_staging_bytes(int collective, int algo, int gs, size_t count, int dtype) {
+  // Mirrors the Binder layouts of do_all_gather / do_reduce_scatter /
+  // do_hier_*; algo 3 = hierarchical. count = AG block / RS chunk elements.
+  const size_t es = dt_size(dtype);
+  if (gs < 1) gs = 1;
+  const size_t full = align256((size_t)gs * count * es), blk = align256(count * es);
+  if (collective == PCCL_ALL_GATHER) return algo == A_DIRECT ? blk : full;
+  if (algo == 3) return 4 * full;
+  return algo == A_DIRECT ? full : 2 * full;
+}
+
+int pccl_comm_create(pccl_world_t w, const int *members, int n, int comm_id, pccl_comm_t *out) {
+  if (!w || !members || !out || n < 1 || n > w->nranks) return PCCL_ERR_INVALID_ARGUMENT;
+  pccl_comm *c = new pccl_comm();
+  c->w = w;
+  c->gs = n;
+  c->comm_id = comm_id;
+  for (int i = 0; i < n; ++i) {
+    if (members[i] < 0 || members[i] >= w->nranks || (c->mask >> members[i]) & 1u) {
+      delete c;
+      return PCCL_ERR_INVALID_ARGUMENT;
+    }
+    c->members[i] = members[i];
+    c->mask |= 1u << members[i];
+    if (!w->emu && members[i] == w->rank) c->gi = i;
+  }
+  if (!w->emu && c->gi < 0) {
+    delete c;
+    return PCCL_ERR_INDEX_OUT_OF_RANGE;
+  }
+  c->slot = slot_for(w, c->mask);
+  if (c->slot < 0) {
+    delete c;
+    return PCCL_ERR_OUT_OF_MEMORY;
+  }
+  *out = c;
+  return PCCL_SUCCESS;
+}
+
+int pccl_comm_destroy(pccl_comm_t c) {
+  if (!c) return PCCL_ERR_INVALID_ARGUMENT;
+  delete c;
+  return PCCL_SUCCESS;
+}
+
+int pccl_comm_size(pccl_comm_t c, int *size) {
+  if (!c || !size) return PCCL_ERR_INVALID_ARGUMENT;
+  *size = c->gs;
+  return PCCL_SUCCESS;
+}
+
+int pccl_comm_rank(pccl_comm_t c, int *rank) {
+  if (!c || !rank) return PCCL_ERR_INVALID_ARGUMENT;
+  *rank = c->gi;
+  return PCCL_SUCCESS;
+}
+
+int pccl_all_gather(pccl_comm_t c, int algo, const void *send, void *recv, size_t count, int dtype, void *stream) {
+  if (!c || c->w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(c->w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_all_gather(c, algo, one(c->w->rank), s, r, count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_reduce_scatter(pccl_comm_t c, int algo, int order, const void *send, void *recv, size_t recvcount, int dtype,
+                        void *stream) {
+  if (!c || c->w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(c->w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_reduce_scatter(c, algo, order, one(c->w->rank), s, r, recvcount, dtype, (cudaStream_t)stream);
+}
+
+int pccl_hier_all_gather(pccl_world_t w, int N, int M, int inter, const void *send, void *recv, size_t count, int dtype,
+                         void *stream) {
+  if (!w || w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_hier_all_gather(w, N, M, inter, one(w->rank), s, r, count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const void *send, void *recv, size_t recvcount,
+                             int dtype, void *stream) {
+  if (!w || w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_hier_reduce_scatter(w, N, M, inter, one(w->rank), s, r, recvcount, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_all_gather(pccl_comm_t c, int algo, const void *const *sends, void *const *recvs, size_t count, int dtype,
+                        void *stream) {
+  if (!c || !c->w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> ranks(c->members, c->members + c->gs);
+  return do_all_gather(c, algo, ranks, sends, recvs, count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_reduce_scatter(pccl_comm_t c, int algo, int order, const void *const *sends, void *const *recvs,
+                            size_t recvcount, int dtype, void *stream) {
+  if (!c || !c->w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> ranks(c->members, c->members + c->gs);
+  return do_reduce_scatter(c, algo, order, ranks, sends, recvs, recvcount, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_hier_all_gather(pccl_world_t w, int N, int M, int inter, const void *const *sends, void *const *recvs,
+                             size_t count, int dtype, void *stream) {
+  if (!w || !w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> ranks;
+  for (int r = 0; r < w->nranks; ++r) ranks.push_back(r);
+  return do_hier_all_gather(w, N, M, inter, ranks, sends, recvs, count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const void *const *sends, void *const *recvs,
+                                 size_t recvcount, int dtype, void *stream) {
+  if (!w || !w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> ranks;
+  for (int r = 0; r < w->nranks; ++r) ranks.push_back(r);
+  return do_hier_reduce_scatter(w, N, M, inter, ranks, sends, recvs, recvcount, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask) {
+  if (!w || rank < 0 || rank >= w->nranks) return PCCL_ERR_INVALID_ARGUMENT;
+  w->meta_skew[rank] = xor_mask & 0x7fffffff;
+  return PCCL_SUCCESS;
+}
+
+int pccl_shuffle(int direction, const void *in, void *out, int N, int M, size_t block_len, int dtype, void *stream) {
+  const size_t es = dt_size(dtype);
+  if (!es || N < 1 || M < 1 || (direction != 0 && direction != 1)) return PCCL_ERR_INVALID_ARGUMENT;
+  const size_t total = (size_t)N * M * block_len * es;
+  if (total == 0) return PCCL_SUCCESS;
+  // direction 0 (local-major -> global): input is an M x N grid -> out N x M
+  const int A = direction == 0 ? N : M;  // output-major dimension
+  const int Bd = direction == 0 ? M : N;
+  uint64_t acc = (uint64_t)(uintptr_t)in | (uint64_t)(uintptr_t)out | (uint64_t)(block_len * es);
+  int U = 16;
+  while (U > 1 && (acc & (uint64_t)(U - 1))) U >>= 1;
+  const int64_t blk = (int64_t)(block_len * es / U);
+  const int64_t units = (int64_t)A * Bd * blk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((units + kThreads - 1) / kThreads, (int64_t)sms * 4);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (U) {
+    case 16: k_shuffle<16><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
+    case 8: k_shuffle<8><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
+    case 4: k_shuffle<4><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
+    case 2: k_shuffle<2><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
+    default: k_shuffle<1><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
+  }
+  CK(cudaGetLastError());
+  return PCCL_SUCCESS;
+}
+
+int pccl_reduce_inplace(void *acc, const void *other, size_t count, int dtype, void *stream) {
+  if (count == 0) return PCCL_SUCCESS;
+  if (!acc || !other) return PCCL_ERR_INVALID_ARGUMENT;
+  const size_t es = dt_size(dtype);
+  const bool vec = (((uintptr_t)acc | (uintptr_t)other | (count * es)) & 15) == 0;
+  const int64_t n = vec ? (int64_t)(count * es / 16) : (int64_t)count;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)sms * 4);
+  cudaStream_t s = (cudaStream_t)stream;
+#define RI(DT)                                                                                      \
+  if (vec) k_reduce_inplace<DT, true><<<grid, kThreads, 0, s>>>((char *)acc, (const char *)other, n); \
+  else k_reduce_inplace<DT, false><<<grid, kThreads, 0, s>>>((char *)acc, (const char *)other, n);
+  switch (dtype) {
+    case PCCL_FLOAT32: RI(DT_F32); break;
+    case PCCL_BFLOAT16: RI(DT_BF16); break;
+    case PCCL_FLOAT16: RI(DT_F16); break;
+    default: return PCCL_ERR_UNSUPPORTED;
+  }
+#undef RI
+  CK(cudaGetLastError());
+  return PCCL_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// schedule introspection: rows (step, src, dst, nbytes) — dst pulls from src
+// ---------------------------------------------------------------------------
+namespace {
+struct Rows {
+  int64_t *rows;
+  int cap, n = 0, step = 0;
+  bool overflow = false;
+  void add(int src, int dst, int64_t bytes) {
+    if (n >= cap) { overflow = true; return; }
+    int64_t *r = rows + 4 * n++;
+    r[0] = step; r[1] = src; r[2] = dst; r[3] = bytes;
+  }
+};
+
+// Emits the steps of one flat collective over `members` (concurrent groups
+// are merged by the caller by resetting `step` to the phase's start).
+int flat_steps(Rows &R, int coll, int algo, const std::vector<int> &mem, int64_t m_bytes, int step0) {
+  const int gs = (int)mem.size();
+  if (m_bytes % gs) return PCCL_ERR_NOT_DIVISIBLE;
+  const int64_t blk = m_bytes / gs;
+  if (gs == 1) return PCCL_SUCCESS;
+  if (algo == A_RING) {
+    for (int s = 0; s < gs - 1; ++s) {
+      R.step = step0 + s;
+      for (int gi = 0; gi < gs; ++gi) R.add(mem[ring_prev(gi, gs)], mem[gi], blk);
+    }
+  } else if (algo == A_REC) {
+    if (!is_pow2(gs)) return PCCL_ERR_NON_POWER_OF_TWO;
+    int L = 0;
+    while ((1 << L) < gs) ++L;
+    for (int k = 0; k < L; ++k) {
+      R.step = step0 + k;
+      for (int gi = 0; gi < gs; ++gi) {
+        if (coll == PCCL_ALL_GATHER) R.add(mem[recdbl_partner(gi, k)], mem[gi], (int64_t)(1 << k) * blk);
+        else R.add(mem[rechalf_partner(gi, gs, k)], mem[gi], (int64_t)(gs >> (k + 1)) * blk);
+      }
+    }
+  } else if (algo == A_DIRECT) {
+    R.step = step0;
+    for (int gi = 0; gi < gs; ++gi)
+      for (int q = 0; q < gs; ++q)
+        if (q != gi) R.add(mem[q], mem[gi], blk);
+  } else {
+    return PCCL_ERR_INVALID_ARGUMENT;
+  }
+  return PCCL_SUCCESS;
+}
+
+int nsteps(int algo, int gs) {
+  if (gs == 1) return 0;
+  if (algo == A_RING) return gs - 1;
+  if (algo == A_DIRECT) return 1;
+  int L = 0;
+  while ((1 << L) < gs) ++L;
+  return L;
+}
+}  // namespace
+
+int pccl_schedule(int coll, int algo, int inter, int N, int M, size_t m_bytes, int64_t *rows, int cap, int *nrows) {
+  if (!rows || !nrows || N < 1 || M < 1 || N * M > PCCL_MAXR) return PCCL_ERR_INVALID_ARGUMENT;
+  Rows R{rows, cap};
+  const int p = N * M;
+  int s = PCCL_SUCCESS;
+  if (algo != 3) {  // flat over the world
+    std::vector<int> mem;
+    for (int g = 0; g < p; ++g) mem.push_back(g);
+    s = flat_steps(R, coll, algo, mem, (int64_t)m_bytes, 0);
+  } else {  // hierarchical: inter phase (groups j) and intra phase (groups n)
+    if ((int64_t)m_bytes % p) return PCCL_ERR_NOT_DIVISIBLE;
+    if (inter == A_REC && !is_pow2(N)) return PCCL_ERR_NON_POWER_OF_TWO;
+    auto inter_phase = [&](int step0) {
+      for (int j = 0; j < M && !s; ++j) {
+        std::vector<int> mem;
+        for (int n = 0; n < N; ++n) mem.push_back(n * M + j);
+        s = flat_steps(R, coll, inter, mem, (int64_t)m_bytes / M, step0);
+      }
+      return step0 + nsteps(inter, N);
+    };
+    auto intra_phase = [&](int step0) {
+      for (int n = 0; n < N && !s; ++n) {
+        std::vector<int> mem;
+        for (int l = 0; l < M; ++l) mem.push_back(n * M + l);
+        s = flat_steps(R, coll, A_RING, mem, (int64_t)m_bytes, step0);
+      }
+      return step0 + nsteps(A_RING, M);
+    };
+    if (coll == PCCL_ALL_GATHER) intra_phase(inter_phase(0));
+    else inter_phase(intra_phase(0));
+  }
+  *nrows = R.n;
+  if (s) return s;
+  return R.overflow ? PCCL_ERR_OUT_OF_MEMORY : PCCL_SUCCESS;
+}
+
+}  // extern "C"

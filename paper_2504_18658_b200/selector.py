@@ -1,0 +1,204 @@
+"""Algorithm selection (mirrors ``collkit/costmodel.py:24-196``).
+
+Two layers:
+
+* the reference's inter-node selector, same contract: ``choose_inter_algorithm``
+  (analytic mode compares the alpha-beta formulas, ring on ties and for
+  non-power-of-two N; table mode looks up a :class:`CalibrationTable`), used
+  by ``HierPlan.resolve_inter``;
+* a flat selector for ``all_gather(..., algorithm="auto")`` /
+  ``reduce_scatter``: a :class:`FlatTable` of *measured* B200 bus bandwidth per
+  (collective, p, message size) — written by ``tools/calibrate.py`` on the GPU
+  box into ``data/flat_calibration.csv`` — with the nearest log-size bucket
+  winning, as in ``CalibrationTable.lookup`` (costmodel.py:127-139).
+
+The default ``CostParams`` describe NVLink 5 on B200 (flag round trip a few
+microseconds; 770 GB/s measured peer copy per direction), not the reference's
+desk-scale defaults, but the analytic selector's decisions are the same:
+with equal per-step bandwidth the recursive variant wins exactly when it has
+fewer steps (pow2 N >= 4), and N = 2 ties go to ring.
+"""
+from __future__ import annotations
+
+import csv
+import math
+import os
+from dataclasses import dataclass, field
+
+from .errors import EmptyTable, NonPowerOfTwo
+
+DATA_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+FLAT_TABLE_PATH = os.path.join(DATA_DIR, "flat_calibration.csv")
+
+
+def _is_pow2(n: int) -> bool:
+    return n >= 1 and (n & (n - 1)) == 0
+
+
+@dataclass(frozen=True)
+class CostParams:
+    alpha_inter: float = 3e-6
+    beta_inter: float = 1.0 / 770e9
+    alpha_intra: float = 3e-6
+    beta_intra: float = 1.0 / 770e9
+    gamma_reduce_fast: float = 1.0 / 6.5e12
+    gamma_reduce_slow: float = 0.4e-9
+    packet_bytes: int = 2048
+
+    def __post_init__(self) -> None:
+        for name in ("alpha_inter", "beta_inter", "alpha_intra", "beta_intra", "gamma_reduce_fast",
+                     "gamma_reduce_slow"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be >= 0")
+        if self.packet_bytes < 1:
+            raise ValueError("packet_bytes must be >= 1")
+
+    def alpha_beta(self, level: str):
+        if level == "inter":
+            return self.alpha_inter, self.beta_inter
+        if level == "intra":
+            return self.alpha_intra, self.beta_intra
+        raise ValueError(f"unknown level {level!r}")
+
+
+def t_ring(p: int, m_bytes: float, params: CostParams, level: str = "inter") -> float:
+    if p < 1:
+        raise ValueError(f"p must be >= 1, got {p}")
+    a, b = params.alpha_beta(level)
+    return a * (p - 1) + b * m_bytes * (p - 1) / p
+
+
+def t_rec(p: int, m_bytes: float, params: CostParams, level: str = "inter") -> float:
+    if not _is_pow2(p):
+        raise NonPowerOfTwo(f"recursive algorithms require power-of-two p, got {p}")
+    a, b = params.alpha_beta(level)
+    return a * math.log2(p) + b * m_bytes * (p - 1) / p
+
+
+def t_direct(p: int, m_bytes: float, params: CostParams, level: str = "intra") -> float:
+    """One step: every peer's share moves concurrently over the switch."""
+    a, b = params.alpha_beta(level)
+    return (a if p > 1 else 0.0) + b * m_bytes * (p - 1) / p
+
+
+@dataclass(frozen=True)
+class CalibrationEntry:
+    n_nodes: int
+    m_bytes: int
+    ring_seconds: float
+    recursive_seconds: float
+    winner: str
+
+
+@dataclass
+class CalibrationTable:
+    entries: list = field(default_factory=list)
+
+    def add(self, entry: CalibrationEntry) -> None:
+        self.entries.append(entry)
+
+    def lookup(self, n_nodes: int, m_bytes: float) -> str:
+        cands = [e for e in self.entries if e.n_nodes == n_nodes]
+        if not cands:
+            raise EmptyTable(f"no calibration entries for N={n_nodes} ({len(self.entries)} entries total)")
+        x = math.log(max(m_bytes, 1.0))
+        return min(cands, key=lambda e: abs(x - math.log(e.m_bytes))).winner
+
+    def save_csv(self, path) -> None:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["N", "m_bytes", "ring_seconds", "recursive_seconds", "winner"])
+            for e in self.entries:
+                w.writerow([e.n_nodes, e.m_bytes, repr(e.ring_seconds), repr(e.recursive_seconds), e.winner])
+
+    @classmethod
+    def load_csv(cls, path) -> "CalibrationTable":
+        t = cls()
+        with open(path, newline="") as fh:
+            for row in csv.DictReader(fh):
+                t.add(CalibrationEntry(int(row["N"]), int(row["m_bytes"]), float(row["ring_seconds"]),
+                                       float(row["recursive_seconds"]), row["winner"]))
+        return t
+
+
+def choose_inter_algorithm(n_nodes: int, m_bytes: float, params: CostParams | None = None,
+                           mode: str = "analytic", table: CalibrationTable | None = None) -> str:
+    """Same contract as costmodel.choose_inter_algorithm (costmodel.py:169-196)."""
+    if n_nodes < 2:
+        raise ValueError(f"selection needs at least 2 nodes, got {n_nodes}")
+    if mode == "table":
+        if table is None or not table.entries:
+            raise EmptyTable("table mode requires a calibration table")
+        return table.lookup(n_nodes, m_bytes)
+    if mode != "analytic":
+        raise ValueError(f"unknown selection mode {mode!r}")
+    if not _is_pow2(n_nodes):
+        return "ring"
+    params = params or CostParams()
+    return "ring" if t_ring(n_nodes, m_bytes, params) <= t_rec(n_nodes, m_bytes, params) else "recursive"
+
+
+# ---------------------------------------------------------------------------
+# flat selector from measured bus bandwidth
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class FlatEntry:
+    collective: str
+    p: int
+    m_bytes: int
+    algorithm: str
+    busbw_gbs: float
+
+
+@dataclass
+class FlatTable:
+    entries: list = field(default_factory=list)
+
+    def add(self, e: FlatEntry) -> None:
+        self.entries.append(e)
+
+    def best(self, collective: str, p: int, m_bytes: float) -> str:
+        cands = [e for e in self.entries if e.collective == collective and e.p == p]
+        if not cands:
+            raise EmptyTable(f"no measurements for {collective} at p={p}")
+        x = math.log(max(m_bytes, 1.0))
+        size = min({e.m_bytes for e in cands}, key=lambda m: abs(x - math.log(m)))
+        return max((e for e in cands if e.m_bytes == size), key=lambda e: e.busbw_gbs).algorithm
+
+    def save_csv(self, path) -> None:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["collective", "p", "m_bytes", "algorithm", "busbw_gbs"])
+            for e in self.entries:
+                w.writerow([e.collective, e.p, e.m_bytes, e.algorithm, f"{e.busbw_gbs:.3f}"])
+
+    @classmethod
+    def load_csv(cls, path) -> "FlatTable":
+        t = cls()
+        with open(path, newline="") as fh:
+            for row in csv.DictReader(fh):
+                t.add(FlatEntry(row["collective"], int(row["p"]), int(row["m_bytes"]), row["algorithm"],
+                                float(row["busbw_gbs"])))
+        return t
+
+
+_flat_table: FlatTable | None = None
+
+
+def flat_table() -> FlatTable | None:
+    global _flat_table
+    if _flat_table is None and os.path.exists(FLAT_TABLE_PATH):
+        _flat_table = FlatTable.load_csv(FLAT_TABLE_PATH)
+    return _flat_table
+
+
+def choose_algorithm(collective: str, p: int, m_bytes: float) -> str:
+    """Measured winner for (collective, p, size); one-shot ``direct`` (the
+    fewest steps over a full-bandwidth switch) when nothing was measured."""
+    t = flat_table()
+    if t is not None:
+        try:
+            return t.best(collective, p, m_bytes)
+        except EmptyTable:
+            pass
+    return "direct"

@@ -1,0 +1,194 @@
+"""Symmetric device memory of one NVSwitch box (host side).
+
+A :class:`World` is the B200 replacement of the reference's transport state
+(``collkit/transport/inprocess.py:14-51``, ``transport/base.py:76-102``): instead
+of queues of byte payloads it owns *segments* of device memory that every rank
+maps (CUDA IPC over NVLink 5 / NVSwitch):
+
+* segment 0 — flag arena (cross-GPU signals, see ``csrc/device.cuh``);
+* staging — where the C layer copies device buffers that peers must read but
+  that the caller did not allocate symmetrically;
+* io — where host (numpy) inputs are uploaded and outputs downloaded, so the
+  drop-in numpy path never pays a device-to-device staging copy;
+* user segments — :meth:`World.empty` returns tensors peers can read
+  zero-copy (the FSDP path keeps parameters / gradients there).
+
+Real mode: one process per GPU; segment handles are exchanged through the
+caller's bootstrap (``exchange(bytes) -> list[bytes]``, normally
+``torch.distributed.all_gather_object``). Emulation mode: ``nranks`` ranks in one
+process on one GPU, every "peer" pointer local; the same kernels run all ranks
+in one cooperative launch.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Callable
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+TORCH_DTYPES = {
+    torch.float32: "f32",
+    torch.bfloat16: "bf16",
+    torch.float16: "f16",
+    torch.uint8: "u8",
+    torch.int32: "i32",
+    torch.int64: "i64",
+    torch.float64: "f64",
+}
+
+
+class _CudaArray:
+    """Minimal ``__cuda_array_interface__`` view of a raw device pointer."""
+
+    def __init__(self, ptr: int, nbytes: int, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,),
+            "typestr": "|u1",
+            "data": (ptr, False),
+            "version": 3,
+            "strides": None,
+        }
+
+
+class Segment:
+    def __init__(self, world: "World", seg_id: int, nbytes: int):
+        self.world = world
+        self.id = seg_id
+        self.nbytes = nbytes
+
+    def ptr(self, rank: int) -> int:
+        p = ctypes.c_void_p()
+        check(lib().pccl_segment_ptr(self.world.handle, self.id, rank, ctypes.byref(p), None), "segment_ptr")
+        return p.value or 0
+
+    def tensor(self, rank: int, offset: int = 0, nbytes: int | None = None) -> torch.Tensor:
+        """uint8 tensor over [offset, offset + nbytes) of rank's copy (this
+        process must own it: its own rank in real mode, any rank in emulation)."""
+        nbytes = self.nbytes - offset if nbytes is None else nbytes
+        base = torch.as_tensor(_CudaArray(self.ptr(rank), self.nbytes, self), device=f"cuda:{self.world.device}")
+        return base[offset : offset + nbytes]
+
+
+class World:
+    """Symmetric memory + flag arena shared by all communicators of a box."""
+
+    def __init__(self, handle: int, nranks: int, rank: int, device: int, emulated: bool,
+                 exchange: Callable[[bytes], list] | None):
+        self.handle = ctypes.c_void_p(handle)
+        self.nranks = nranks
+        self.rank = rank
+        self.device = device
+        self.emulated = emulated
+        self._exchange = exchange
+        self._segments: dict[int, Segment] = {}
+        self.staging: Segment | None = None
+        self.io: Segment | None = None
+        self.lock = threading.RLock()
+        self._closed = False
+        self._share(0, 0)  # flag arena
+
+    # ---- construction -------------------------------------------------
+    @classmethod
+    def create(cls, nranks: int, rank: int, device: int, exchange: Callable[[bytes], list]) -> "World":
+        h = ctypes.c_void_p()
+        check(lib().pccl_world_create(nranks, rank, device, ctypes.byref(h)), "world_create")
+        return cls(h.value, nranks, rank, device, False, exchange)
+
+    @classmethod
+    def emulated_world(cls, nranks: int, device: int = 0) -> "World":
+        h = ctypes.c_void_p()
+        check(lib().pccl_emu_world_create(nranks, device, ctypes.byref(h)), "emu_world_create")
+        return cls(h.value, nranks, -1, device, True, None)
+
+    # ---- segments -------------------------------------------------------
+    def _share(self, seg_id: int, nbytes: int) -> Segment:
+        """Export/exchange/import segment seg_id (collective in real mode)."""
+        if not self.emulated:
+            buf = (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+            check(lib().pccl_segment_export(self.handle, seg_id, buf), "segment_export")
+            handles = self._exchange(bytes(buf))
+            if len(handles) != self.nranks:
+                raise RuntimeError("bootstrap exchange returned the wrong number of handles")
+            allh = (ctypes.c_char * (_lib.IPC_HANDLE_BYTES * self.nranks))()
+            for q, hb in enumerate(handles):
+                ctypes.memmove(ctypes.addressof(allh) + q * _lib.IPC_HANDLE_BYTES, hb, _lib.IPC_HANDLE_BYTES)
+            check(lib().pccl_segment_import(self.handle, seg_id, allh), "segment_import")
+        seg = Segment(self, seg_id, nbytes)
+        self._segments[seg_id] = seg
+        return seg
+
+    def create_segment(self, nbytes: int) -> Segment:
+        """Collective (real mode): allocate nbytes on every rank and map them."""
+        sid = ctypes.c_int(-1)
+        check(lib().pccl_segment_create(self.handle, nbytes, ctypes.byref(sid)), "segment_create")
+        return self._share(sid.value, nbytes)
+
+    def destroy_segment(self, seg: Segment) -> None:
+        torch.cuda.synchronize(self.device)
+        check(lib().pccl_segment_destroy(self.handle, seg.id), "segment_destroy")
+        self._segments.pop(seg.id, None)
+
+    @staticmethod
+    def _grow(need: int) -> int:
+        size = 1 << 20
+        while size < need:
+            size <<= 1
+        return size
+
+    def ensure_staging(self, nbytes: int) -> None:
+        """Collective over the world when it grows (all ranks ask for the same size)."""
+        with self.lock:
+            if self.staging is not None and self.staging.nbytes >= nbytes:
+                return
+            if self.staging is not None:
+                self.destroy_segment(self.staging)
+            self.staging = self.create_segment(self._grow(nbytes))
+            check(lib().pccl_world_set_staging(self.handle, self.staging.id), "set_staging")
+
+    def ensure_io(self, nbytes: int) -> Segment:
+        with self.lock:
+            if self.io is None or self.io.nbytes < nbytes:
+                if self.io is not None:
+                    self.destroy_segment(self.io)
+                self.io = self.create_segment(self._grow(nbytes))
+            return self.io
+
+    def empty(self, numel: int, dtype=torch.float32, rank: int | None = None):
+        """Symmetric tensor(s) peers can read zero-copy. Collective in real
+        mode (returns this rank's tensor); in emulation returns one tensor per
+        rank."""
+        es = torch.empty(0, dtype=dtype).element_size()
+        seg = self.create_segment(max(256, numel * es))
+        if self.emulated:
+            return [seg.tensor(r, 0, numel * es).view(dtype) for r in range(self.nranks)]
+        return seg.tensor(self.rank, 0, numel * es).view(dtype)
+
+    # ---- status --------------------------------------------------------
+    def check(self) -> None:
+        """Raise a device-reported error (Timeout, LengthMismatch, ...)."""
+        check(lib().pccl_world_check(self.handle), "device")
+
+    def reset_flags(self) -> None:
+        check(lib().pccl_world_reset_flags(self.handle), "reset_flags")
+
+    def set_tuning(self, ctas: int = 0, nsub: int = 0) -> None:
+        check(lib().pccl_world_set_tuning(self.handle, ctas, nsub, 0), "set_tuning")
+
+    def set_timeout_ms(self, ms: int) -> None:
+        check(lib().pccl_world_set_timeout_ms(self.handle, ms), "set_timeout")
+
+    def close(self) -> None:
+        if not self._closed and self.handle:
+            self._closed = True
+            lib().pccl_world_destroy(self.handle)
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,12 @@
+"""Test configuration: the `gpu` marker and the repo root on sys.path."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu)")
+    config.addinivalue_line("markers", "multigpu: needs >= 2 GPUs on one box")

@@ -1,0 +1,115 @@
+"""Real-mode parity worker: one process per GPU (launched by torchrun from
+tests/test_gpu_multiproc.py). Every rank builds the same seeded inputs for all
+ranks, runs each collective through the public API over CUDA-IPC peer memory,
+and checks its own output bit-for-bit against the oracle (test
+infrastructure). Exit code 0 = all checks passed on this rank."""
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+
+
+def main() -> int:
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    import paper_2504_18658_b200 as pkg
+
+    comm = pkg.init_from_torch()
+    p = world
+    failures = []
+
+    def check(name, got, want):
+        g = np.ascontiguousarray(got)
+        w = np.ascontiguousarray(want)
+        if g.shape != w.shape or not np.array_equal(g.view(np.uint8), w.view(np.uint8)):
+            failures.append(name)
+
+    rng = np.random.default_rng(1234)
+    pow2 = p & (p - 1) == 0
+    for n in (1, 37, 4096, 300_000):
+        ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+        rs_in = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+        want_ag = oracle.ring_all_gather(ag_in)[rank]
+        algos = [("ring", pkg.ring_all_gather), ("direct", pkg.direct_all_gather)]
+        if pow2:
+            algos.append(("recursive", pkg.recdbl_all_gather))
+        for name, fn in algos:
+            check(f"ag_{name}_n{n}", fn(comm, ag_in[rank]), want_ag)
+        check(f"rs_ring_n{n}", pkg.ring_reduce_scatter(comm, rs_in[rank]), oracle.ring_reduce_scatter(rs_in)[rank])
+        check(f"rs_direct_ring_n{n}", pkg.direct_reduce_scatter(comm, rs_in[rank], order="ring"),
+              oracle.ring_reduce_scatter(rs_in)[rank])
+        if pow2:
+            want = oracle.rechalf_reduce_scatter(rs_in)[rank]
+            check(f"rs_rechalf_n{n}", pkg.rechalf_reduce_scatter(comm, rs_in[rank]), want)
+            check(f"rs_direct_rec_n{n}", pkg.direct_reduce_scatter(comm, rs_in[rank], order="recursive"), want)
+
+    # bf16 on device tensors, both through staging and through symmetric buffers
+    n = 65536 + 8
+    ins = [oracle.f32_to_bf16(rng.standard_normal(n * p).astype(np.float32)) for _ in range(p)]
+    dev_in = torch.from_numpy(ins[rank].view(np.int16)).view(torch.bfloat16).cuda()
+    sym_in = comm.world.empty(n * p, torch.bfloat16)
+    sym_in.copy_(dev_in)
+    sym_out = comm.world.empty(n, torch.bfloat16)
+    for algo, ref in [("ring", oracle.ring_reduce_scatter)] + ([("recursive", oracle.rechalf_reduce_scatter)] if pow2 else []):
+        want = ref(ins, "bf16")[rank]
+        got = pkg.reduce_scatter(comm, dev_in, algorithm=algo)
+        check(f"bf16_{algo}_staged", got.view(torch.int16).cpu().numpy().view(np.uint16), want)
+        got = pkg.reduce_scatter(comm, sym_in, algorithm=algo, out=sym_out)
+        check(f"bf16_{algo}_symmetric", got.view(torch.int16).cpu().numpy().view(np.uint16), want)
+    want = oracle.direct_reduce_scatter(ins, "bf16", "ring")[rank]
+    got = pkg.reduce_scatter(comm, sym_in, algorithm="direct", out=sym_out)
+    check("bf16_direct_symmetric", got.view(torch.int16).cpu().numpy().view(np.uint16), want)
+
+    # hierarchical virtual nodes
+    grids = [(N, p // N) for N in (1, 2, 4, 8) if p % N == 0]
+    for N, M in grids:
+        for inter in ("ring", "recursive"):
+            if inter == "recursive" and N & (N - 1):
+                continue
+            plan = pkg.HierPlan(topo=pkg.Topology(N, M), inter_alg=inter)
+            ag_in = [rng.standard_normal(1000).astype(np.float32) for _ in range(p)]
+            check(f"hier_ag_{N}x{M}_{inter}", pkg.hier_all_gather(plan, comm, ag_in[rank]),
+                  oracle.hier_all_gather(ag_in, N, M, inter)[rank])
+            rs_in = [rng.standard_normal(1000 * p).astype(np.float32) for _ in range(p)]
+            check(f"hier_rs_{N}x{M}_{inter}", pkg.hier_reduce_scatter(plan, comm, rs_in[rank]),
+                  oracle.hier_reduce_scatter(rs_in, N, M, inter)[rank])
+
+    # back-to-back reuse + barrier
+    for it in range(30):
+        x = torch.full((4096 * p,), float(it + rank), device="cuda")
+        y = pkg.reduce_scatter(comm, x, algorithm=["direct", "ring", "recursive" if pow2 else "ring"][it % 3])
+        if float(y[0]) != sum(it + q for q in range(p)):
+            failures.append(f"reuse_{it}")
+    comm.barrier()
+
+    # cross-rank length mismatch must raise LengthMismatch (device-side check)
+    from paper_2504_18658_b200.errors import LengthMismatch
+
+    try:
+        pkg.direct_all_gather(comm, np.zeros(4 if rank == 0 else 2, np.float32))
+        failures.append("mismatch_not_detected")
+    except LengthMismatch:
+        pass
+
+    torch.cuda.synchronize()
+    print(f"[rank {rank}] {'OK' if not failures else 'FAIL ' + ','.join(failures)}", flush=True)
+    return 1 if failures else 0
+
+
+if __name__ == "__main__":
+    try:
+        code = main()
+    except Exception:
+        traceback.print_exc()
+        code = 2
+    os._exit(code)

@@ -1,0 +1,319 @@
+"""GPU parity tests, emulation mode: p ranks of one process on cuda:0, every
+collective ONE cooperative launch of the same kernels the multi-GPU path runs
+(peer pointers are local). Called through the reference-shaped public API
+(``run_ranks`` + ``ring_all_gather(comm, buf)`` ...), checked bit-for-bit
+against golden vectors produced by the real reference (collkit) and against
+the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.golden import fixtures
+
+pytestmark = pytest.mark.gpu
+
+P = None  # imported lazily so collection works without the library
+
+
+def _pkg():
+    global P
+    if P is None:
+        import paper_2504_18658_b200 as pkg
+
+        P = pkg
+    return P
+
+
+CASES = fixtures.cases()
+Z = fixtures.arrays()
+
+
+def _flat_fn(op, algo):
+    pkg = _pkg()
+    return {
+        ("ag", "ring"): pkg.ring_all_gather,
+        ("ag", "recursive"): pkg.recdbl_all_gather,
+        ("rs", "ring"): pkg.ring_reduce_scatter,
+        ("rs", "recursive"): pkg.rechalf_reduce_scatter,
+    }[(op, algo)]
+
+
+def _bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["algo"] != "hierarchical"], ids=lambda c: c["name"])
+def test_flat_matches_reference_golden(case):
+    pkg = _pkg()
+    ins = Z[case["name"] + "/in"]
+    want = Z[case["name"] + "/out"]
+    p = case["p"]
+    fn = _flat_fn(case["op"], case["algo"])
+    outs = pkg.run_ranks(p, lambda c: fn(c, ins[c.rank]))
+    for r in range(p):
+        assert outs[r].dtype == np.float32
+        assert _bits_equal(outs[r], want[r]), (case["name"], r)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["algo"] != "hierarchical"], ids=lambda c: c["name"])
+def test_direct_matches_reference_golden(case):
+    """One-shot kernels: AG identical; RS folded in the named algorithm's
+    order is bit-identical to that algorithm's reference output."""
+    pkg = _pkg()
+    ins = Z[case["name"] + "/in"]
+    want = Z[case["name"] + "/out"]
+    p = case["p"]
+    if case["op"] == "ag":
+        outs = pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, ins[c.rank]))
+    else:
+        outs = pkg.run_ranks(p, lambda c: pkg.direct_reduce_scatter(c, ins[c.rank], order=case["algo"]))
+    for r in range(p):
+        assert _bits_equal(outs[r], want[r]), (case["name"], r)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["algo"] == "hierarchical"], ids=lambda c: c["name"])
+def test_hierarchical_matches_reference_golden(case):
+    pkg = _pkg()
+    ins = Z[case["name"] + "/in"]
+    want = Z[case["name"] + "/out"]
+    N, M = case["N"], case["M"]
+    plan = pkg.HierPlan(topo=pkg.Topology(N, M), inter_alg=case["inter"])
+    fn = pkg.hier_all_gather if case["op"] == "ag" else pkg.hier_reduce_scatter
+    outs = pkg.run_ranks(N * M, lambda c: fn(plan, c, ins[c.rank]))
+    for r in range(N * M):
+        assert _bits_equal(outs[r], want[r]), (case["name"], r)
+
+
+# ---------------------------------------------------------------------------
+# low precision: bit-exact against the oracle's wire semantics, and within the
+# stated tolerance of the exact sum
+# ---------------------------------------------------------------------------
+def _bf16_inputs(p, n, seed):
+    rng = np.random.default_rng(seed)
+    return [oracle.f32_to_bf16(rng.standard_normal(n * p).astype(np.float32)) for _ in range(p)]
+
+
+def _to_dev(bits, dtype):
+    t = torch.from_numpy(bits.view(np.int16) if dtype == torch.bfloat16 else bits)
+    return t.view(dtype).cuda()
+
+
+def _from_dev(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("p", [2, 4, 8, 16])
+@pytest.mark.parametrize("algo", ["ring", "recursive", "direct"])
+@pytest.mark.parametrize("n", [8, 1000, 4096 + 24])
+def test_bf16_reduce_scatter(p, algo, n):
+    pkg = _pkg()
+    ins = _bf16_inputs(p, n, seed=p * 1000 + n)
+    fns = {
+        "ring": pkg.ring_reduce_scatter,
+        "recursive": pkg.rechalf_reduce_scatter,
+        "direct": lambda c, x: pkg.direct_reduce_scatter(c, x, order="ring"),
+    }
+    outs = pkg.run_ranks(p, lambda c: _from_dev(fns[algo](c, _to_dev(ins[c.rank], torch.bfloat16))))
+    if algo == "direct":
+        want = oracle.direct_reduce_scatter(ins, "bf16", "ring")
+    else:
+        want = (oracle.ring_reduce_scatter if algo == "ring" else oracle.rechalf_reduce_scatter)(ins, "bf16")
+    # exact float64 sum for the tolerance bound |y - s| <= p * 2^-8 * sum|x|
+    f = [oracle.bf16_to_f32(x).astype(np.float64) for x in ins]
+    for r in range(p):
+        assert np.array_equal(outs[r], want[r]), (algo, p, r)
+        exact = sum(x[r * n : (r + 1) * n] for x in f)
+        mag = sum(np.abs(x[r * n : (r + 1) * n]) for x in f)
+        err = np.abs(oracle.bf16_to_f32(outs[r]).astype(np.float64) - exact)
+        assert np.all(err <= p * 2.0**-8 * mag + 1e-30)
+
+
+@pytest.mark.parametrize("p", [2, 8])
+@pytest.mark.parametrize("algo", ["ring", "recursive", "direct"])
+def test_f16_reduce_scatter(p, algo):
+    pkg = _pkg()
+    rng = np.random.default_rng(p)
+    n = 520
+    ins = [rng.standard_normal(n * p).astype(np.float16) for _ in range(p)]
+    fns = {
+        "ring": pkg.ring_reduce_scatter,
+        "recursive": pkg.rechalf_reduce_scatter,
+        "direct": lambda c, x: pkg.direct_reduce_scatter(c, x, order="recursive"),
+    }
+    outs = pkg.run_ranks(p, lambda c: fns[algo](c, torch.from_numpy(ins[c.rank]).cuda()).cpu().numpy())
+    if algo == "direct":
+        want = oracle.direct_reduce_scatter(ins, "f16", "recursive")
+    else:
+        want = (oracle.ring_reduce_scatter if algo == "ring" else oracle.rechalf_reduce_scatter)(ins, "f16")
+    for r in range(p):
+        assert _bits_equal(outs[r], want[r])
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.int64, torch.uint8, torch.float64])
+@pytest.mark.parametrize("algo", ["ring", "recursive", "direct"])
+def test_all_gather_any_dtype_byte_exact(dtype, algo):
+    pkg = _pkg()
+    p, n = 8, 333
+    g = torch.Generator().manual_seed(5)
+    ins = [torch.randint(0, 200, (n,), generator=g).to(dtype) for _ in range(p)]
+    fn = {"ring": pkg.ring_all_gather, "recursive": pkg.recdbl_all_gather, "direct": pkg.direct_all_gather}[algo]
+    outs = pkg.run_ranks(p, lambda c: fn(c, ins[c.rank].cuda()).cpu())
+    want = torch.cat(ins)
+    for r in range(p):
+        assert outs[r].dtype == dtype and torch.equal(outs[r], want)
+
+
+# ---------------------------------------------------------------------------
+# large sizes: size-independent properties (vectorised, pipelined path)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("algo", ["ring", "recursive", "direct"])
+def test_large_fp32_integer_sums_exact(p, algo):
+    """Integer-valued fp32 (the reference's test domain) sums are exact in any
+    order: RS chunks must equal the exact sum; AG must reassemble the inputs."""
+    pkg = _pkg()
+    n = (1 << 20) + 96
+    g = torch.Generator().manual_seed(p)
+    ins = [torch.randint(-1024, 1025, (n * p,), generator=g).float().cuda() for _ in range(p)]
+    rs = {"ring": pkg.ring_reduce_scatter, "recursive": pkg.rechalf_reduce_scatter,
+          "direct": pkg.direct_reduce_scatter}[algo]
+    outs = pkg.run_ranks(p, lambda c: rs(c, ins[c.rank]))
+    total = sum(x.double() for x in ins)
+    for r in range(p):
+        assert torch.equal(outs[r].double(), total[r * n : (r + 1) * n])
+    ag = {"ring": pkg.ring_all_gather, "recursive": pkg.recdbl_all_gather, "direct": pkg.direct_all_gather}[algo]
+    outs = pkg.run_ranks(p, lambda c: ag(c, ins[c.rank][:n]))
+    want = torch.cat([x[:n] for x in ins])
+    for r in range(p):
+        assert torch.equal(outs[r], want)
+
+
+@pytest.mark.parametrize("p", [4, 8])
+def test_large_fp32_normal_bit_exact_vs_oracle(p):
+    pkg = _pkg()
+    n = 300_000
+    rng = np.random.default_rng(99)
+    ins = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    for algo, fn, ref in [
+        ("ring", pkg.ring_reduce_scatter, oracle.ring_reduce_scatter),
+        ("recursive", pkg.rechalf_reduce_scatter, oracle.rechalf_reduce_scatter),
+    ]:
+        outs = pkg.run_ranks(p, lambda c: fn(c, ins[c.rank]))
+        want = ref(ins)
+        for r in range(p):
+            assert _bits_equal(outs[r], want[r]), (algo, r)
+
+
+def test_back_to_back_calls_reuse_buffers():
+    """Epoch flags never reset: many consecutive calls stay correct."""
+    pkg = _pkg()
+    p, n = 8, 50_000
+    g = torch.Generator().manual_seed(3)
+
+    def body(c):
+        res = []
+        for it in range(20):
+            x = torch.full((n * p,), float(it + c.rank), device="cuda")
+            algo = ["direct", "ring", "recursive"][it % 3]
+            y = pkg.reduce_scatter(c, x, algorithm=algo)
+            res.append(float(y[0].item()))
+        return res
+
+    outs = pkg.run_ranks(p, body)
+    for r in range(p):
+        for it in range(20):
+            assert outs[r][it] == sum(it + q for q in range(p))
+
+
+# ---------------------------------------------------------------------------
+# edge cases and errors (reference contract)
+# ---------------------------------------------------------------------------
+def test_p1_returns_copy():
+    pkg = _pkg()
+    x = np.array([5.0], np.float32)
+    out = pkg.run_ranks(1, lambda c: pkg.ring_all_gather(c, x))
+    assert np.array_equal(out[0], [5.0]) and out[0] is not x
+
+
+def test_empty_payloads():
+    pkg = _pkg()
+    for fn in (pkg.ring_all_gather, pkg.recdbl_all_gather, pkg.direct_all_gather):
+        outs = pkg.run_ranks(4, lambda c: fn(c, np.zeros(0, np.float32)))
+        assert all(o.size == 0 for o in outs)
+    outs = pkg.run_ranks(4, lambda c: pkg.ring_reduce_scatter(c, np.zeros(0, np.float32)))
+    assert all(o.size == 0 for o in outs)
+
+
+def test_errors():
+    pkg = _pkg()
+    from paper_2504_18658_b200.errors import LengthMismatch, NonPowerOfTwo, NotDivisible
+
+    with pytest.raises(NotDivisible):
+        pkg.run_ranks(2, lambda c: pkg.ring_reduce_scatter(c, np.zeros(3, np.float32)))
+    with pytest.raises(NonPowerOfTwo):
+        pkg.run_ranks(3, lambda c: pkg.recdbl_all_gather(c, np.zeros(2, np.float32)))
+    with pytest.raises(NonPowerOfTwo):
+        pkg.run_ranks(6, lambda c: pkg.rechalf_reduce_scatter(c, np.zeros(12, np.float32)))
+    sizes = [4, 2]
+    with pytest.raises(LengthMismatch):
+        pkg.run_ranks(2, lambda c: pkg.ring_all_gather(c, np.zeros(sizes[c.rank], np.float32)))
+    # still usable afterwards
+    outs = pkg.run_ranks(2, lambda c: pkg.ring_all_gather(c, np.full(2, c.rank, np.float32)))
+    assert np.array_equal(outs[1], [0, 0, 1, 1])
+
+
+@pytest.mark.parametrize("algo", ["direct", "ring", "recursive"])
+def test_device_side_signature_mismatch_aborts_cleanly(algo):
+    """A rank whose call signature differs (what a cross-rank size mismatch
+    looks like on a real multi-GPU job) must make every rank raise
+    LengthMismatch via the device flag protocol — not hang."""
+    pkg = _pkg()
+    from paper_2504_18658_b200 import _lib
+    from paper_2504_18658_b200.errors import LengthMismatch
+
+    w = pkg.emulated_world(4)
+    _lib.lib().pccl_emu_debug_meta_skew(w.handle, 2, 0x1234)
+    try:
+        with pytest.raises(LengthMismatch):
+            pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(4096, device="cuda"), algorithm=algo))
+    finally:
+        _lib.lib().pccl_emu_debug_meta_skew(w.handle, 2, 0)
+        w.reset_flags()
+    outs = pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(4096, device="cuda"), algorithm=algo))
+    assert all(torch.all(o == 4) for o in outs)
+
+
+def test_shuffles_match_reference_golden():
+    pkg = _pkg()
+    for key in [k[: -len("/in")] for k in Z.files if k.startswith("shuffle_") and k.endswith("/in")]:
+        dims, b = key[len("shuffle_"):].split("_b")
+        N, M = map(int, dims.split("x"))
+        buf = Z[key + "/in"]
+        assert np.array_equal(pkg.shuffle_local_major_to_global(buf, N, M, int(b)), Z[key + "/l2g"])
+        assert np.array_equal(pkg.shuffle_global_to_local_major(buf, N, M, int(b)), Z[key + "/g2l"])
+
+
+def test_reduce_inplace_matches_scalar_loop():
+    pkg = _pkg()
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(64).astype(np.float32)
+    b = rng.standard_normal(64).astype(np.float32)
+    want = np.array([float(a[i]) + float(b[i]) for i in range(64)], dtype=np.float32)
+    acc = a.copy()
+    assert pkg.reduce_inplace(acc, b) is acc
+    assert np.array_equal(acc, want)
+
+
+def test_hier_block_trace_and_all_ones():
+    pkg = _pkg()
+    plan = pkg.HierPlan(topo=pkg.Topology(2, 2), inter_alg="ring")
+    outs = pkg.run_ranks(4, lambda c: pkg.hier_all_gather(plan, c, np.array([float(c.rank)], np.float32)))
+    assert all(np.array_equal(o, [0, 1, 2, 3]) for o in outs)
+    outs = pkg.run_ranks(4, lambda c: pkg.hier_reduce_scatter(pkg.HierPlan(topo=pkg.Topology(2, 2)), c,
+                                                              np.ones(4, np.float32)))
+    assert all(np.array_equal(o, [4.0]) for o in outs)
