@@ -96,6 +96,12 @@ int pccl_world_check(pccl_world_t w);           /* device-reported error, then c
 int pccl_world_reset_flags(pccl_world_t w);      /* zero flags + epochs (emulation, after an error) */
 int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
+/* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "nsub" (pipeline
+ * sub-slices), "ag_variant" / "rs_variant" (data movement: 0 pull = LDG from
+ * peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push), "tma_stages",
+ * "tma_tile", "timeout_ms". Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
+int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
+int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
 
 /* ---- symmetric segments ---------------------------------------------- */
 int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id);

@@ -36,6 +36,8 @@ _SIGS = {
     "pccl_world_reset_flags": (_i, [_vp]),
     "pccl_world_set_tuning": (_i, [_vp, _i, _i, _i]),
     "pccl_world_set_timeout_ms": (_i, [_vp, ctypes.c_int64]),
+    "pccl_world_set_param": (_i, [_vp, ctypes.c_char_p, ctypes.c_int64]),
+    "pccl_world_get_param": (_i, [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
     "pccl_segment_create": (_i, [_vp, _sz, ctypes.POINTER(_i)]),
     "pccl_segment_export": (_i, [_vp, _i, _vp]),
     "pccl_segment_import": (_i, [_vp, _i, _vp]),

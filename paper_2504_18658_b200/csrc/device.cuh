@@ -28,7 +28,7 @@
 #ifndef PCCL_MAXR
 #define PCCL_MAXR 16
 #endif
-#define PCCL_MAX_CTAS 128
+#define PCCL_MAX_CTAS 160
 #define PCCL_NSLOTS 256
 #define PCCL_SLOT_WORDS (3 * PCCL_MAXR * PCCL_MAX_CTAS)
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
@@ -54,7 +54,10 @@ struct LaunchParams {
   int local_copy;   // AG: copy own send block into recv
   int order;        // direct RS fold order
   int skip_exit;    // 1: no DONE barrier (buffers not reused while peers read)
-  int pad0;
+  int variant;      // data-movement variant (experiments / tuning)
+  int tma_stages;   // TMA ring depth
+  uint32_t tma_tile;  // TMA tile bytes
+  int pad1;
   int64_t timeout_ns;
   int64_t blk;              // units per sub-block
   int64_t sub_stride;       // stride between sub-blocks (shared layout)
@@ -448,6 +451,112 @@ __device__ __forceinline__ void reduce2_units(char *dst, const char *a, const ch
     acc_add<typename R::Acc, R::N>(s, R::load(ld_peer(y + i)));
     d[i] = R::store(s);
   }
+}
+
+
+// --------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk) + mbarriers: one elected thread moves large
+// tiles between global memory (local or NVLink-mapped peer) and shared memory
+// with almost no instruction overhead, so a few SMs keep MBs in flight.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void tma_load(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store(void *gdst, const void *smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// A per-CTA ring of S shared-memory stages of T bytes driven by one thread.
+struct TmaRing {
+  char *buf;
+  uint64_t *full;
+  int S;
+  uint32_t T;
+  uint32_t n;  // tiles issued so far (stage = n % S, parity = (n / S) & 1)
+};
+
+// One thread: copy the concatenation of segments (dst[i] <- src[i], len[i]
+// bytes, multiples of 16) through the ring, keeping S-1 tile loads in flight.
+// Returns after every store has *completed* (safe to publish with a flag).
+template <typename SegFn>
+__device__ __forceinline__ void tma_copy_segments(TmaRing &R, int nseg, SegFn seg) {
+  // flatten tiles lazily: walk segments with (i, off)
+  int li = 0, si = 0;          // load cursor (segment, offset) / store cursor
+  int64_t loff = 0, soff = 0;
+  char *d; const char *s; int64_t len;
+  auto next_tile = [&](int &i, int64_t &off, char *&dd, const char *&ss, uint32_t &bytes) -> bool {
+    while (i < nseg) {
+      seg(i, dd, ss, len);
+      if (off < len) {
+        { const int64_t rem = len - off; bytes = rem < (int64_t)R.T ? (uint32_t)rem : R.T; }
+        dd += off;
+        ss += off;
+        off += bytes;
+        return true;
+      }
+      ++i;
+      off = 0;
+    }
+    return false;
+  };
+  const uint32_t base = R.n;
+  uint32_t issued = 0, retired = 0;
+  char *ld; const char *ls; uint32_t lb;
+  // prologue
+  while (issued < (uint32_t)R.S && next_tile(li, loff, ld, ls, lb)) {
+    const uint32_t k = base + issued;
+    uint64_t *bar = R.full + (k % R.S);
+    mbar_expect_tx(bar, lb);
+    tma_load(R.buf + (size_t)(k % R.S) * R.T, ls, lb, bar);
+    ++issued;
+  }
+  while (retired < issued) {
+    const uint32_t k = base + retired;
+    const int st = k % R.S;
+    mbar_wait(R.full + st, (k / R.S) & 1);
+    char *sd; const char *ss2; uint32_t sb;
+    next_tile(si, soff, sd, ss2, sb);
+    tma_store(sd, R.buf + (size_t)st * R.T, sb);
+    tma_commit();
+    ++retired;
+    if (next_tile(li, loff, ld, ls, lb)) {
+      tma_wait_read_all();  // stage st free again
+      const uint32_t k2 = base + issued;
+      uint64_t *bar = R.full + (k2 % R.S);
+      mbar_expect_tx(bar, lb);
+      tma_load(R.buf + (size_t)(k2 % R.S) * R.T, ls, lb, bar);
+      ++issued;
+    }
+  }
+  R.n = base + issued;
+  tma_wait_all();
+  fence_proxy_async();
 }
 
 }  // namespace pccl

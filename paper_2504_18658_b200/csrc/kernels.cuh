@@ -125,6 +125,109 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
   cta_exit(c, partners, partners);
 }
 
+
+// ============================================================================
+// direct all-gather data-movement variants (P.variant):
+//   0 LDG pull (k_ag_direct), 1 STG push, 2 TMA pull, 3 TMA push.
+// Push variants write into the peers' (symmetric) recv: the entry handshake
+// means "my recv may be overwritten", the second one "my block has landed".
+// ============================================================================
+template <int U>
+__device__ __forceinline__ void store_units(char *dst, const char *src, int64_t lo, int64_t hi) {
+  using T = typename VecT<U>::T;
+  T *d = reinterpret_cast<T *>(dst);
+  const T *s = reinterpret_cast<const T *>(src);
+  const int nt = blockDim.x;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (int64_t)(kUnroll - 1) * nt < hi; i += (int64_t)kUnroll * nt) {
+    T v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = __ldg(s + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) d[i + (int64_t)u * nt] = v[u];
+  }
+  for (; i < hi; i += nt) d[i] = __ldg(s + i);
+}
+
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
+  cta_publish_meta(c, peers);
+  cta_signal_mask(c, peers, 0);  // my recv may be written
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  if (P.local_copy) ag_local_copy<U>(c, lo, hi);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  for (int i = 1; i < c.gs; ++i) {
+    const int q = (c.gi + i) % c.gs;
+    char *dst = P.recv[c.world(q)];
+    for (int t = 0; t < P.nsubblk; ++t)
+      store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
+  }
+  cta_signal_mask(c, peers, 1);  // my block has landed in your recv
+  if (!cta_wait_mask(c, peers, 1, false)) return;
+}
+
+struct TmaCfg {
+  static constexpr int kMaxStages = 8;
+};
+
+__device__ __forceinline__ TmaRing tma_ring_setup(char *dsm, int S, uint32_t T) {
+  TmaRing R;
+  R.buf = dsm;
+  R.full = reinterpret_cast<uint64_t *>(dsm + (size_t)S * T);
+  R.S = S;
+  R.T = T;
+  R.n = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(R.full + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  return R;
+}
+
+template <bool PUSH>
+__global__ void __launch_bounds__(kThreads) k_ag_direct_tma(const __grid_constant__ LaunchParams P) {
+  extern __shared__ __align__(128) char dsm[];
+  Ctx c = make_ctx(P);
+  const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
+  TmaRing R = tma_ring_setup(dsm, P.tma_stages, P.tma_tile);
+  cta_publish_meta(c, peers);
+  cta_signal_mask(c, peers, 0);
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    const int gs = c.gs, nsb = P.nsubblk;
+    const int nseg = gs * nsb;  // segment 0..nsb-1: own block (local copy)
+    tma_copy_segments(R, nseg, [&](int i, char *&d, const char *&s, int64_t &len) {
+      const int k = i / nsb, t = i % nsb;
+      const int q = (c.gi + k) % gs;
+      len = (hi - lo) * 16;
+      if (k == 0) {
+        if (!P.local_copy) { len = 0; d = nullptr; s = nullptr; return; }
+        d = ag_block<16>(P, P.recv[c.r], c.y, c.gi, t) + lo * 16;
+        s = P.send[c.r] + ((int64_t)t * P.send_sub_stride + lo) * 16;
+      } else if (PUSH) {
+        d = ag_block<16>(P, P.recv[c.world(q)], c.y, c.gi, t) + lo * 16;
+        s = P.send[c.r] + ((int64_t)t * P.send_sub_stride + lo) * 16;
+      } else {
+        d = ag_block<16>(P, P.recv[c.r], c.y, q, t) + lo * 16;
+        s = P.send[c.world(q)] + ((int64_t)t * P.send_sub_stride + lo) * 16;
+      }
+    });
+  }
+  if (PUSH) {
+    cta_signal_mask(c, peers, 1);
+    if (!cta_wait_mask(c, peers, 1, false)) return;
+  } else {
+    cta_exit(c, peers, peers);
+  }
+}
+
 // ============================================================================
 // reduce-scatter
 // ============================================================================
@@ -203,11 +306,27 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
   cta_exit(c, partners, partners);
 }
 
-// Direct reduce-scatter: every member's chunk `gi` is pulled in one step and
-// folded in registers in the named order. Leaves are loaded first (MAXP
-// independent 16-byte loads in flight per thread), then combined with static
-// register indices.
-template <int DT, bool VEC, int ORDER, int MAXP>
+// Direct reduce-scatter, one step. PULL: every member's chunk `gi` is read
+// from the peers' symmetric send buffers. PUSH: every rank first stores its
+// chunk q into member q's staging slot [gi] (posted NVLink writes), then folds
+// its own slots locally. Either way the leaves are loaded first (MAXP
+// independent 16-byte loads in flight per thread) and combined with static
+// register indices in the named order.
+template <typename T>
+__device__ __forceinline__ void copy_typed(T *d, const T *s, int64_t lo, int64_t hi) {
+  const int nt = blockDim.x;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (int64_t)(kUnroll - 1) * nt < hi; i += (int64_t)kUnroll * nt) {
+    T v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = __ldg(s + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) d[i + (int64_t)u * nt] = v[u];
+  }
+  for (; i < hi; i += nt) d[i] = __ldg(s + i);
+}
+
+template <int DT, bool VEC, int ORDER, int MAXP, bool PUSH>
 __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ LaunchParams P) {
   using R = RUnit<DT, VEC>;
   using T = typename R::T;
@@ -216,11 +335,20 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   const int gs = c.gs, gi = c.gi;
   const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
   cta_publish_meta(c, peers);
-  cta_signal_mask(c, peers, 0);
+  cta_signal_mask(c, peers, 0);  // pull: my send is ready; push: my staging is free
   if (!cta_wait_mask(c, peers, 0, true)) return;
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  // source member of leaf position i
+  const T *own = reinterpret_cast<const T *>(P.send[c.r]);
+  if (PUSH) {
+    for (int i = 1; i < gs; ++i) {
+      const int q = (gi + i) % gs;
+      T *dst = reinterpret_cast<T *>(P.work[c.world(q)]) + (int64_t)gi * P.blk;
+      copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
+    }
+    cta_signal_mask(c, peers, 1);  // my chunks have landed
+    if (!cta_wait_mask(c, peers, 1, false)) return;
+  }
   const T *src[MAXP];
 #pragma unroll
   for (int i = 0; i < MAXP; ++i) {
@@ -229,11 +357,15 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
     else if (ORDER == O_REC) q = gi ^ i;
     else q = i;
     if (i >= gs) q = gi;
-    src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]);
+    if (PUSH)
+      src[i] = (q == gi) ? own + P.base[c.y] + (int64_t)gi * P.istride
+                         : reinterpret_cast<const T *>(P.work[c.r]) + (int64_t)q * P.blk;
+    else
+      src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]) + P.base[c.y] + (int64_t)gi * P.istride;
   }
   const int nt = blockDim.x;
   for (int j = 0; j < P.nsubblk; ++j) {
-    const int64_t off = P.base[c.y] + (int64_t)gi * P.istride + (int64_t)j * P.sub_stride;
+    const int64_t off = (int64_t)j * P.sub_stride;
     T *dst = reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
     for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
       T raw[MAXP];
@@ -267,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
       dst[e] = R::store(acc);
     }
   }
-  cta_exit(c, peers, peers);
+  if (!PUSH) cta_exit(c, peers, peers);
 }
 
 // ============================================================================

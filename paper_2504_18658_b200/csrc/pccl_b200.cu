@@ -40,10 +40,14 @@ struct pccl_world {
   uint64_t epoch[PCCL_NSLOTS] = {};
   std::map<uint32_t, int> slot_of_mask;  // emulation: dynamic slot allocation
   int sms = 148;
-  int ctas = 0;      // 0: auto
-  int nsub = 4;
-  int threads = kThreads;
-  int64_t timeout_ns = 20ll * 1000 * 1000 * 1000;
+  // tuning knobs (pccl_world_set_param)
+  int64_t p_ctas = 0;  // 0: auto
+  int64_t p_nsub = 1;
+  int64_t p_ag_variant = 0;
+  int64_t p_rs_variant = 0;
+  int64_t p_tma_stages = 3;
+  int64_t p_tma_tile = 65536;
+  int64_t p_timeout_ms = 20000;
   uint32_t meta_skew[PCCL_MAXR] = {};
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
 };
@@ -147,19 +151,17 @@ KernelFn ag_kernel(int algo, int U) {
   return nullptr;
 }
 
-template <int DT, bool VEC>
-KernelFn rs_kernel_dt(int algo, int order, int maxp) {
-  if (algo == A_RING) return (KernelFn)k_rs_ring<DT, VEC>;
-  if (algo == A_REC) return (KernelFn)k_rs_rec<DT, VEC>;
-#define RSD(O)                                                   \
-  if (order == O) {                                              \
-    if (!VEC) return (KernelFn)k_rs_direct<DT, VEC, O, 16>;      \
-    switch (maxp) {                                              \
-      case 2: return (KernelFn)k_rs_direct<DT, VEC, O, 2>;       \
-      case 4: return (KernelFn)k_rs_direct<DT, VEC, O, 4>;       \
-      case 8: return (KernelFn)k_rs_direct<DT, VEC, O, 8>;       \
-      default: return (KernelFn)k_rs_direct<DT, VEC, O, 16>;     \
-    }                                                            \
+template <int DT, bool VEC, bool PUSH>
+KernelFn rs_direct_kernel(int order, int maxp) {
+#define RSD(O)                                                          \
+  if (order == O) {                                                     \
+    if (!VEC) return (KernelFn)k_rs_direct<DT, VEC, O, 16, PUSH>;       \
+    switch (maxp) {                                                     \
+      case 2: return (KernelFn)k_rs_direct<DT, VEC, O, 2, PUSH>;        \
+      case 4: return (KernelFn)k_rs_direct<DT, VEC, O, 4, PUSH>;        \
+      case 8: return (KernelFn)k_rs_direct<DT, VEC, O, 8, PUSH>;        \
+      default: return (KernelFn)k_rs_direct<DT, VEC, O, 16, PUSH>;      \
+    }                                                                   \
   }
   RSD(O_RING)
   RSD(O_REC)
@@ -168,10 +170,20 @@ KernelFn rs_kernel_dt(int algo, int order, int maxp) {
   return nullptr;
 }
 
-KernelFn rs_kernel(int dt, bool vec, int algo, int order, int maxp) {
-  if (dt == PCCL_FLOAT32) return vec ? rs_kernel_dt<DT_F32, true>(algo, order, maxp) : rs_kernel_dt<DT_F32, false>(algo, order, maxp);
-  if (dt == PCCL_BFLOAT16) return vec ? rs_kernel_dt<DT_BF16, true>(algo, order, maxp) : rs_kernel_dt<DT_BF16, false>(algo, order, maxp);
-  if (dt == PCCL_FLOAT16) return vec ? rs_kernel_dt<DT_F16, true>(algo, order, maxp) : rs_kernel_dt<DT_F16, false>(algo, order, maxp);
+template <int DT, bool VEC>
+KernelFn rs_kernel_dt(int algo, int order, int maxp, int variant) {
+  if (algo == A_RING) return (KernelFn)k_rs_ring<DT, VEC>;
+  if (algo == A_REC) return (KernelFn)k_rs_rec<DT, VEC>;
+  return variant == 1 ? rs_direct_kernel<DT, VEC, true>(order, maxp) : rs_direct_kernel<DT, VEC, false>(order, maxp);
+}
+
+KernelFn rs_kernel(int dt, bool vec, int algo, int order, int maxp, int variant) {
+#define RSK(D)                                                                                              \
+  return vec ? rs_kernel_dt<D, true>(algo, order, maxp, variant) : rs_kernel_dt<D, false>(algo, order, maxp, variant);
+  if (dt == PCCL_FLOAT32) { RSK(DT_F32) }
+  if (dt == PCCL_BFLOAT16) { RSK(DT_BF16) }
+  if (dt == PCCL_FLOAT16) { RSK(DT_F16) }
+#undef RSK
   return nullptr;
 }
 
@@ -199,6 +211,7 @@ struct Plan {
   // per world rank buffers
   char *send[PCCL_MAXR] = {}, *recv[PCCL_MAXR] = {}, *work[PCCL_MAXR] = {}, *out[PCCL_MAXR] = {};
   uint32_t place = 0;  // symmetric-placement hash (real mode)
+  int variant = 0;
 };
 
 int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
@@ -209,9 +222,12 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.nsubblk = pl.nsubblk;
   P.local_copy = pl.local_copy;
   P.order = pl.order;
-  P.timeout_ns = w->timeout_ns;
+  P.timeout_ns = (w->p_timeout_ms * 1000000ll);
   P.err = w->err_dev;
-  P.nsub = std::max(1, std::min(w->nsub, 64));
+  P.nsub = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_nsub, 64));
+  P.variant = pl.variant;
+  P.tma_stages = (int)w->p_tma_stages;
+  P.tma_tile = (uint32_t)w->p_tma_tile;
 
   // ---- unit size: largest power of two dividing every byte offset/pointer
   const int64_t bytes_terms[] = {pl.blk * (int64_t)es, pl.sub_stride * (int64_t)es, pl.istride * (int64_t)es,
@@ -227,17 +243,32 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   }
   int U;  // bytes per unit
   KernelFn k;
+  size_t smem = 0;
   if (pl.coll == PCCL_ALL_GATHER) {
     U = 16;
     while (U > 1 && (acc & (uint64_t)(U - 1))) U >>= 1;
     if ((size_t)U < es && es <= 16 && !(acc & (es - 1))) U = (int)es;
     k = ag_kernel(pl.algo, U);
+    if (pl.algo == A_DIRECT && (pl.variant == 1 || pl.variant == 3))
+      k = U == 16 ? (KernelFn)k_ag_direct_push<16> : (KernelFn)k_ag_direct_push<1>;
+    if (pl.algo == A_DIRECT && (pl.variant == 1 || pl.variant == 3) && U != 16) {
+      switch (U) {
+        case 8: k = (KernelFn)k_ag_direct_push<8>; break;
+        case 4: k = (KernelFn)k_ag_direct_push<4>; break;
+        case 2: k = (KernelFn)k_ag_direct_push<2>; break;
+        default: break;
+      }
+    }
+    if (pl.algo == A_DIRECT && U == 16 && (pl.variant == 2 || pl.variant == 3)) {
+      k = pl.variant == 2 ? (KernelFn)k_ag_direct_tma<false> : (KernelFn)k_ag_direct_tma<true>;
+      smem = (size_t)w->p_tma_stages * w->p_tma_tile + 8 * (size_t)w->p_tma_stages;
+    }
   } else {
     const bool vec = (acc & 15ull) == 0;
     U = vec ? 16 : (int)es;
     int maxp = 2;
     while (maxp < pl.gs) maxp <<= 1;
-    k = rs_kernel(pl.dtype, vec, pl.algo, pl.order, maxp);
+    k = rs_kernel(pl.dtype, vec, pl.algo, pl.order, maxp, pl.variant);
   }
   if (!k) return PCCL_ERR_UNSUPPORTED;
   const int64_t epu = U / (int64_t)es > 0 ? U / (int64_t)es : 1;  // elements per unit
@@ -279,19 +310,23 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
 
   // ---- grid
   const int threads = kThreads;
-  int ctas = w->ctas > 0 ? w->ctas : (w->emu ? 16 : 32);
+  int ctas = w->p_ctas > 0 ? (int)w->p_ctas : (w->emu ? 16 : 128);
   ctas = std::min(ctas, PCCL_MAX_CTAS);
-  if (w->emu) {
-    const int cap = max_coresident((const void *)k, threads, w->sms);
+  {
+    int per_sm = 0;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, threads, smem));
+    const int cap = std::max(1, per_sm) * w->sms;  // every CTA must be co-resident (they wait on each other)
     ctas = std::max(1, std::min(ctas, cap / nrows));
   }
   P.ctas = ctas;
   dim3 grid(ctas, nrows), block(threads);
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (w->emu) {
     void *args[] = {&P};
-    CK(cudaLaunchCooperativeKernel((const void *)k, grid, block, args, 0, stream));
+    CK(cudaLaunchCooperativeKernel((const void *)k, grid, block, args, smem, stream));
   } else {
-    k<<<grid, block, 0, stream>>>(P);
+    k<<<grid, block, smem, stream>>>(P);
     CK(cudaGetLastError());
   }
   return PCCL_SUCCESS;
@@ -401,6 +436,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.blk = (int64_t)count;
   pl.istride = (int64_t)count;
   pl.send_sub_stride = (int64_t)count;
+  pl.variant = algo == A_DIRECT ? (int)w->p_ag_variant : 0;
   Binder B{w, stream};
   std::vector<std::pair<char *, char *>> copy_out;  // (staged recv, user recv)
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -411,7 +447,14 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
     if (gi < 0) return PCCL_ERR_INDEX_OUT_OF_RANGE;
     pl.rows.push_back({r, c});
     B.cursor = 0;
-    if (algo == A_DIRECT) {
+    if (algo == A_DIRECT && (pl.variant == 1 || pl.variant == 3)) {
+      // push: I write into my peers' recv; send is read locally only
+      char *staged = nullptr;
+      if (!B.symmetric(r, recvs[i], gs * blk_bytes, false, pl.recv, &staged)) return B.status;
+      if (staged) copy_out.push_back({staged, (char *)recvs[i]});
+      pl.send[r] = (char *)sends[i];
+      pl.local_copy = staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+    } else if (algo == A_DIRECT) {
       // peers read my send; my recv is written locally only
       if (!B.symmetric(r, sends[i], blk_bytes, true, pl.send, nullptr)) return B.status;
       pl.recv[r] = (char *)recvs[i];
@@ -459,6 +502,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.blk = (int64_t)recvcount;
   pl.istride = (int64_t)recvcount;
   pl.out_sub_stride = (int64_t)recvcount;
+  pl.variant = algo == A_DIRECT ? (int)w->p_rs_variant : 0;
   Binder B{w, stream};
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
@@ -467,6 +511,13 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     if (!member) return PCCL_ERR_INDEX_OUT_OF_RANGE;
     pl.rows.push_back({r, c});
     B.cursor = 0;
+    if (pl.variant == 1) {
+      // push: send is read locally only; peers write into my staging slots
+      pl.send[r] = (char *)sends[i];
+      if (!B.scratch(r, gs * chunk_bytes, pl.work)) return B.status;
+      pl.out[r] = (char *)recvs[i];
+      continue;
+    }
     if (!B.symmetric(r, sends[i], gs * chunk_bytes, true, pl.send, nullptr)) return B.status;
     if (algo != A_DIRECT) {
       B.cursor = align256(gs * chunk_bytes);  // work at the same offset on every rank
@@ -682,9 +733,13 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   memset(h, 0, 64);
   w->err_host = (volatile int *)h;
   CK(cudaHostGetDevicePointer((void **)&w->err_dev, h, 0));
-  if (const char *t = getenv("PCCL_TIMEOUT_MS")) w->timeout_ns = atoll(t) * 1000000ll;
-  if (const char *t = getenv("PCCL_CTAS")) w->ctas = atoi(t);
-  if (const char *t = getenv("PCCL_NSUB")) w->nsub = atoi(t);
+  if (const char *t = getenv("PCCL_TIMEOUT_MS")) w->p_timeout_ms = atoll(t);
+  if (const char *t = getenv("PCCL_CTAS")) w->p_ctas = atoi(t);
+  if (const char *t = getenv("PCCL_NSUB")) w->p_nsub = atoi(t);
+  if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
+  if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
+  if (const char *t = getenv("PCCL_TMA_STAGES")) w->p_tma_stages = atoi(t);
+  if (const char *t = getenv("PCCL_TMA_TILE")) w->p_tma_tile = atoi(t);
   int seg = -1;
   int s = pccl_segment_create(w, PCCL_FLAG_BYTES, &seg);
   if (s) return s;
@@ -743,15 +798,48 @@ int pccl_world_reset_flags(pccl_world_t w) {
 
 int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads) {
   if (!w || ctas < 0 || ctas > PCCL_MAX_CTAS || nsub < 0 || nsub > 64) return PCCL_ERR_INVALID_ARGUMENT;
-  w->ctas = ctas;
-  if (nsub) w->nsub = nsub;
+  w->p_ctas = ctas;
+  if (nsub) w->p_nsub = nsub;
   (void)threads;
   return PCCL_SUCCESS;
 }
 
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms) {
   if (!w || ms <= 0) return PCCL_ERR_INVALID_ARGUMENT;
-  w->timeout_ns = ms * 1000000ll;
+  w->p_timeout_ms = ms;
+  return PCCL_SUCCESS;
+}
+
+static int64_t *param_ref(pccl_world *w, const char *key) {
+  if (!strcmp(key, "ctas")) return &w->p_ctas;
+  if (!strcmp(key, "nsub")) return &w->p_nsub;
+  if (!strcmp(key, "ag_variant")) return &w->p_ag_variant;
+  if (!strcmp(key, "rs_variant")) return &w->p_rs_variant;
+  if (!strcmp(key, "tma_stages")) return &w->p_tma_stages;
+  if (!strcmp(key, "tma_tile")) return &w->p_tma_tile;
+  if (!strcmp(key, "timeout_ms")) return &w->p_timeout_ms;
+  return nullptr;
+}
+
+int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
+  if (!w || !key) return PCCL_ERR_INVALID_ARGUMENT;
+  int64_t *ref = param_ref(w, key);
+  if (!ref || value < 0) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "nsub") && (value < 1 || value > 64)) return PCCL_ERR_INVALID_ARGUMENT;
+  if ((!strcmp(key, "ag_variant") || !strcmp(key, "rs_variant")) && value > 3) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;
+  *ref = value;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value) {
+  if (!w || !key || !value) return PCCL_ERR_INVALID_ARGUMENT;
+  int64_t *ref = param_ref(w, key);
+  if (!ref) return PCCL_ERR_INVALID_ARGUMENT;
+  *value = *ref;
   return PCCL_SUCCESS;
 }
 
@@ -846,7 +934,7 @@ size_t pccl_staging_bytes(int collective, int algo, int gs, size_t count, int dt
   const size_t es = dt_size(dtype);
   if (gs < 1) gs = 1;
   const size_t full = align256((size_t)gs * count * es), blk = align256(count * es);
-  if (collective == PCCL_ALL_GATHER) return algo == A_DIRECT ? blk : full;
+  if (collective == PCCL_ALL_GATHER) return full + blk;
   if (algo == 3) return 4 * full;
   return algo == A_DIRECT ? full : 2 * full;
 }

@@ -179,6 +179,15 @@ class World:
     def set_tuning(self, ctas: int = 0, nsub: int = 0) -> None:
         check(lib().pccl_world_set_tuning(self.handle, ctas, nsub, 0), "set_tuning")
 
+    def set_param(self, key: str, value: int) -> None:
+        """Tuning knob (ctas, nsub, ag_variant, rs_variant, tma_stages, tma_tile, timeout_ms)."""
+        check(lib().pccl_world_set_param(self.handle, key.encode(), int(value)), f"set_param({key})")
+
+    def get_param(self, key: str) -> int:
+        v = ctypes.c_int64()
+        check(lib().pccl_world_get_param(self.handle, key.encode(), ctypes.byref(v)), f"get_param({key})")
+        return v.value
+
     def set_timeout_ms(self, ms: int) -> None:
         check(lib().pccl_world_set_timeout_ms(self.handle, ms), "set_timeout")
 

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--colls", default="ag_f32,rs_bf16")
     ap.add_argument("--algos", default="direct,ring,recursive")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--variants", default="0")
+    ap.add_argument("--tma", default="4x32768", help="stages x tile bytes list, comma separated")
     args = ap.parse_args()
     rank = int(os.environ["RANK"])
     p = int(os.environ["WORLD_SIZE"])
@@ -54,7 +56,20 @@ def main():
                 continue
             a = _lib.ALGOS[algo]
             world.ensure_staging(int(L.pccl_staging_bytes(0 if kind == "ag" else 1, a, p, n, code)))
-            for ctas in map(int, args.ctas.split(",")):
+            combos = []
+            for v in map(int, args.variants.split(",")):
+                if v and algo != "direct":
+                    continue
+                if v >= 2 and kind == "rs":
+                    continue
+                for tm in (args.tma.split(",") if v >= 2 else ["0x0"]):
+                    combos.append((v, *map(int, tm.split("x"))))
+            for (variant, stg, tile) in combos:
+              world.set_param("ag_variant" if kind == "ag" else "rs_variant", variant)
+              if stg:
+                  world.set_param("tma_stages", stg)
+                  world.set_param("tma_tile", tile)
+              for ctas in map(int, args.ctas.split(",")):
                 for nsub in map(int, args.nsub.split(",")):
                     world.set_tuning(ctas, nsub)
                     if kind == "ag":
@@ -80,10 +95,13 @@ def main():
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     us = float(t) * 1e3
                     bw = S * (p - 1) / p / (us * 1e-6) / 1e9
-                    results.append(dict(coll=coll, algo=algo, ctas=ctas, nsub=nsub, us=round(us, 1), busbw=round(bw, 1)))
+                    results.append(dict(coll=coll, algo=algo, variant=variant, stages=stg, tile=tile, ctas=ctas,
+                                        nsub=nsub, us=round(us, 1), busbw=round(bw, 1)))
                     if rank == 0:
-                        print(f"p={p} {coll:8s} {algo:9s} ctas={ctas:4d} nsub={nsub:2d} {us:9.1f} us {bw:7.1f} GB/s",
-                              flush=True)
+                        print(f"p={p} {coll:8s} {algo:9s} v={variant} tma={stg}x{tile:6d} ctas={ctas:4d} nsub={nsub:2d} "
+                              f"{us:9.1f} us {bw:7.1f} GB/s", flush=True)
+              world.set_param("ag_variant", 0)
+              world.set_param("rs_variant", 0)
     # NCCL reference points
     for coll in args.colls.split(","):
         kind, dt = coll.split("_")
