@@ -1,0 +1,191 @@
+"""CPU: host-side logic that does not need a GPU — topology/groups, plans,
+selectors, the emulation rendezvous, and the multi-process bootstrap exchange
+(world_size 2 over gloo, 127.0.0.1)."""
+import os
+import threading
+
+import pytest
+
+from paper_2504_18658_b200 import errors
+from paper_2504_18658_b200.communicator import Rendezvous
+from paper_2504_18658_b200.hierarchy import BlockLayout, HierPlan, inter_comm_id, intra_comm_id
+from paper_2504_18658_b200.selector import (
+    CalibrationEntry,
+    CalibrationTable,
+    CostParams,
+    FlatEntry,
+    FlatTable,
+    choose_inter_algorithm,
+    t_rec,
+    t_ring,
+)
+from paper_2504_18658_b200.topology import (
+    RankId,
+    Topology,
+    build_topology,
+    inter_node_group,
+    intra_node_group,
+    nic_of,
+)
+
+
+def test_topology_groups_match_reference_examples():
+    # SPEC.md topology examples
+    t = Topology(2, 2, 1)
+    assert inter_node_group(t, 0).members == (0, 2)
+    assert inter_node_group(t, 1).members == (1, 3)
+    assert intra_node_group(t, 1).members == (2, 3)
+    assert intra_node_group(Topology(1, 4, 1), 0).members == (0, 1, 2, 3)
+    with pytest.raises(errors.IndexOutOfRange):
+        inter_node_group(Topology(3, 2, 1), 2)
+    with pytest.raises(errors.IndexOutOfRange):
+        intra_node_group(t, 2)
+    with pytest.raises(errors.InvalidTopology):
+        build_topology(2, 8, 3)
+    assert build_topology(2, 8, 4).world_size == 16
+    t8 = Topology(2, 8, 4)
+    assert [nic_of(t8, g) for g in range(8)] == [0, 0, 1, 1, 2, 2, 3, 3]
+    assert RankId.of(t8, 13) == RankId(13, 1, 5)
+    # node-major numbering; groups partition the world
+    for N, M in [(2, 4), (4, 2), (1, 8), (8, 1)]:
+        t = Topology(N, M)
+        inter = sorted(g for j in range(M) for g in inter_node_group(t, j).members)
+        intra = sorted(g for n in range(N) for g in intra_node_group(t, n).members)
+        assert inter == intra == list(range(N * M))
+
+
+def test_comm_ids_follow_reference():
+    t = Topology(2, 4)
+    assert [inter_comm_id(t, j) for j in range(4)] == [1, 2, 3, 4]
+    assert [intra_comm_id(t, n) for n in range(2)] == [5, 6]
+
+
+def test_plan_validation_and_auto_resolution():
+    with pytest.raises(errors.NonPowerOfTwo):
+        HierPlan(topo=Topology(3, 2), inter_alg="recursive")
+    with pytest.raises(ValueError):
+        HierPlan(topo=Topology(2, 2), inter_alg="tree")
+    with pytest.raises(ValueError):
+        HierPlan(topo=Topology(2, 2), collective="broadcast")
+    assert HierPlan(topo=Topology(2, 2)).resolve_inter(1 << 20) == "ring"     # tie -> ring
+    assert HierPlan(topo=Topology(64, 2)).resolve_inter(1 << 20) == "recursive"
+    assert HierPlan(topo=Topology(3, 2)).resolve_inter(1 << 20) == "ring"     # non-pow2
+    assert HierPlan(topo=Topology(1, 8)).resolve_inter(1 << 20) == "ring"     # single node
+    table = CalibrationTable()
+    table.add(CalibrationEntry(4, 1 << 20, 1.0, 2.0, "ring"))
+    assert HierPlan(topo=Topology(4, 2), selector_mode="table", table=table).resolve_inter(1 << 20) == "ring"
+    with pytest.raises(errors.EmptyTable):
+        HierPlan(topo=Topology(4, 2), selector_mode="table", table=CalibrationTable()).resolve_inter(1)
+    layout = BlockLayout(block_count=8, block_len=16, ordering="local_major")
+    assert layout.total_elems == 128
+    with pytest.raises(ValueError):
+        BlockLayout(8, 16, "diagonal")
+
+
+def test_cost_model_properties():
+    P = CostParams()
+    for p in (2, 4, 8, 16):
+        for m in (1 << 10, 1 << 20, 1 << 28):
+            assert t_ring(p, m, P) >= t_rec(p, m, P)          # equal bandwidth term, more steps
+            assert t_ring(p, 2 * m, P) > t_ring(p, m, P)       # monotone in size
+    with pytest.raises(errors.NonPowerOfTwo):
+        t_rec(6, 100, P)
+    assert choose_inter_algorithm(2, 1 << 20, P) == "ring"
+    assert choose_inter_algorithm(8, 1 << 20, P) == "recursive"
+
+
+def test_calibration_tables_roundtrip(tmp_path):
+    t = CalibrationTable()
+    t.add(CalibrationEntry(4, 1 << 20, 1e-3, 2e-3, "ring"))
+    t.add(CalibrationEntry(4, 1 << 26, 3e-3, 2e-3, "recursive"))
+    path = tmp_path / "cal.csv"
+    t.save_csv(path)
+    t2 = CalibrationTable.load_csv(path)
+    assert t2.entries == t.entries
+    assert t2.lookup(4, 1 << 25) == "recursive"
+    ft = FlatTable()
+    ft.add(FlatEntry("all_gather", 8, 1 << 26, "direct", 600.0))
+    ft.add(FlatEntry("all_gather", 8, 1 << 26, "ring", 500.0))
+    ft.add(FlatEntry("all_gather", 8, 1 << 20, "ring", 100.0))
+    ft.add(FlatEntry("all_gather", 8, 1 << 20, "direct", 90.0))
+    fp = tmp_path / "flat.csv"
+    ft.save_csv(fp)
+    ft2 = FlatTable.load_csv(fp)
+    assert ft2.best("all_gather", 8, 1 << 27) == "direct"
+    assert ft2.best("all_gather", 8, 1 << 19) == "ring"
+    with pytest.raises(errors.EmptyTable):
+        ft2.best("reduce_scatter", 8, 1)
+
+
+def test_rendezvous_runs_once_and_distributes():
+    rdv = Rendezvous(timeout=10)
+    calls = []
+    out = [None] * 4
+
+    def execute(payloads):
+        calls.append(list(payloads))
+        return [x * 10 for x in payloads]
+
+    def worker(r):
+        for it in range(5):
+            out[r] = rdv.arrive(("k", it), 4, r, r + it, execute)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert len(calls) == 5 and out == [(r + 4) * 10 for r in range(4)]
+
+
+def test_rendezvous_reuses_keys_safely_and_propagates_errors():
+    rdv = Rendezvous(timeout=10)
+    errs = []
+
+    def execute(payloads):
+        raise errors.LengthMismatch("sizes differ")
+
+    def worker(r):
+        try:
+            rdv.arrive("same", 2, r, r, execute)
+        except errors.LengthMismatch:
+            errs.append(r)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert sorted(errs) == [0, 1]
+    with pytest.raises(errors.Timeout):
+        Rendezvous(timeout=0.2).arrive("lonely", 2, 0, None, execute)
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the bootstrap exchange init_from_torch uses for IPC handles
+    blob = bytes([rank]) * 64
+    out = [None] * world
+    dist.all_gather_object(out, blob)
+    q.put((rank, [o[0] for o in out], all(len(o) == 64 for o in out)))
+    dist.destroy_process_group()
+
+
+def test_bootstrap_exchange_world_size_2_gloo():
+    """Handles are exchanged in rank order over the process group (the only
+    host-side collective the GPU path performs)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, [0, 1], True), (1, [0, 1], True)]
