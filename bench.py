@@ -243,7 +243,7 @@ def run_gpu(args):
     # ---- soak (for the clock sampler), warmup, timed region ----
     clocks = Clocks(local_rank)
     with clocks:
-        t_end = time.time() + 1.0
+        t_end = time.time() + (0.0 if args.profile else 1.0)
         while time.time() < t_end:
             for _ in range(20):
                 call()
@@ -324,7 +324,7 @@ def run_gpu(args):
             extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
 
     # ---- e2e through the public API with host buffers ----
-    e2e = run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)
+    e2e = None if args.profile else run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)
 
     # ---- roofline of the dominant kernel (the measured call itself) ----
     pk, src = peaks()
@@ -471,9 +471,12 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if measured")
+    ap.add_argument("--profile", action="store_true", help="minimal launches for ncu: no soak/extra/e2e/cpu")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.profile:
+        args.no_extra = args.no_cpu = True
     if args.impl == "reference":
         run_reference(args)
     else:

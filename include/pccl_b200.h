@@ -155,6 +155,11 @@ int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter_algo, c
  * cross-rank check must raise LengthMismatch (tests/test_collectives.py:172-175). */
 int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask);
 
+/* Debug probe: raw NVLink throughput without any synchronisation. mode 0:
+ * this rank stores `bytes` into each peer in dst_mask (second half of their
+ * segment seg_id), mode 1: loads from them. */
+int pccl_probe(pccl_world_t w, int seg_id, int mode, uint32_t dst_mask, size_t bytes, int ctas, void *stream);
+
 /* ---- device-local helpers ----------------------------------------------- */
 /* direction 0: shuffle_local_major_to_global, 1: shuffle_global_to_local_major
  * (hierarchy.py:103-126); out-of-place block transpose of N*M blocks. */

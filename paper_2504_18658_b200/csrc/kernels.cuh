@@ -402,6 +402,44 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   if (!PUSH) cta_exit(c, peers, peers);
 }
 
+
+// ============================================================================
+// raw NVLink probe (debug): every CTA streams 16-byte vectors to (push) or
+// from (pull) the peers in dst_mask, round-robin by CTA; no flags, no order.
+// ============================================================================
+__global__ void __launch_bounds__(kThreads) k_probe(char *local, const LaunchParams P, uint32_t dst_mask, int64_t units,
+                                                    int mode) {
+  int peers[PCCL_MAXR], np = 0;
+  for (int q = 0; q < PCCL_MAXR; ++q)
+    if ((dst_mask >> q) & 1u) peers[np++] = q;
+  if (np == 0) return;
+  const int q = peers[blockIdx.x % np];
+  const int per_peer_ctas = (gridDim.x + np - 1 - (blockIdx.x % np)) / np;
+  const int idx = blockIdx.x / np;
+  int64_t lo, hi;
+  split32(units, per_peer_ctas, idx, lo, hi);
+  uint4 *rem = reinterpret_cast<uint4 *>(P.recv[q]);
+  uint4 *loc = reinterpret_cast<uint4 *>(local);
+  const int nt = blockDim.x;
+  if (mode == 0) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) v[u] = __ldg(loc + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) rem[i + u * nt] = v[u];
+    }
+  } else {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) v[u] = __ldcg(rem + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) loc[i + u * nt] = v[u];
+    }
+  }
+}
+
 // ============================================================================
 // device-local helpers
 // ============================================================================

@@ -1060,6 +1060,21 @@ int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask) {
   return PCCL_SUCCESS;
 }
 
+int pccl_probe(pccl_world_t w, int seg_id, int mode, uint32_t dst_mask, size_t bytes, int ctas, void *stream) {
+  if (!w || w->emu || seg_id <= 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || bytes % 16 || ctas < 1) return PCCL_ERR_INVALID_ARGUMENT;
+  const Segment &S = w->segs[seg_id];
+  if (2 * bytes > S.bytes) return PCCL_ERR_INVALID_ARGUMENT;
+  LaunchParams P;
+  memset(&P, 0, sizeof(P));
+  // peers' second half is the remote target; my first half is the local side
+  for (int q = 0; q < w->nranks; ++q) P.recv[q] = S.ptr[q] ? S.ptr[q] + S.bytes / 2 : nullptr;
+  dst_mask &= ~(1u << w->rank);
+  CK(cudaSetDevice(w->device));
+  k_probe<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(S.ptr[w->rank], P, dst_mask, (int64_t)(bytes / 16), mode);
+  CK(cudaGetLastError());
+  return PCCL_SUCCESS;
+}
+
 int pccl_shuffle(int direction, const void *in, void *out, int N, int M, size_t block_len, int dtype, void *stream) {
   const size_t es = dt_size(dtype);
   if (!es || N < 1 || M < 1 || (direction != 0 && direction != 1)) return PCCL_ERR_INVALID_ARGUMENT;
