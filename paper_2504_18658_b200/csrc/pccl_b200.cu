@@ -310,7 +310,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
 
   // ---- grid
   const int threads = kThreads;
-  int ctas = w->p_ctas > 0 ? (int)w->p_ctas : (w->emu ? 16 : 128);
+  int ctas = w->p_ctas > 0 ? (int)w->p_ctas : (w->emu ? PCCL_MAX_CTAS : 128);
   ctas = std::min(ctas, PCCL_MAX_CTAS);
   {
     int per_sm = 0;
