@@ -96,12 +96,16 @@ int pccl_world_check(pccl_world_t w);           /* device-reported error, then c
 int pccl_world_reset_flags(pccl_world_t w);      /* zero flags + epochs (emulation, after an error) */
 int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
-/* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "nsub" (pipeline
- * sub-slices), "ag_variant" / "rs_variant" (data movement: 0 pull = LDG from
- * peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push), "tma_stages",
- * "tma_tile", "timeout_ms". Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
+/* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "threads" (per
+ * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
+ * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push), "tma_stages",
+ * "tma_tile", "timeout_ms", "trace". Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
 int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
+/* With param "trace" = 1, every launch records per-CTA events (globaltimer ns
+ * << 16 | kind << 12 | unit; kind 1 start, 2 wait done, 3 signal, 4 end),
+ * 128 words per CTA, laid out [row][cta][event]; copies the last launch's. */
+int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas);
 
 /* ---- symmetric segments ---------------------------------------------- */
 int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id);

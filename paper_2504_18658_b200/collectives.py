@@ -93,14 +93,22 @@ class _In:
         return self.t.numel() * self.t.element_size()
 
 
-def _finish(arg: _In, result: torch.Tensor):
+def _download(results: list) -> list:
+    """Device results -> fresh pinned host tensors, one sync for all."""
+    outs = []
+    for r in results:
+        h = torch.empty(r.shape, dtype=r.dtype, pin_memory=True)
+        h.copy_(r, non_blocking=True)
+        outs.append(h)
+    if results:
+        torch.cuda.current_stream(results[0].device).synchronize()
+    return outs
+
+
+def _finish(arg: _In, host: torch.Tensor):
     """Return in the caller's type: numpy for numpy input, host tensor for a
-    host tensor, the device tensor otherwise (fresh, caller-owned)."""
-    if arg.numpy:
-        return result.cpu().numpy().copy() if result.is_cuda else result.numpy().copy()
-    if arg.host:
-        return result.cpu()
-    return result
+    host tensor (fresh, caller-owned)."""
+    return host.numpy() if arg.numpy else host
 
 
 def _check_world_size_growth(comm, need: int, what: str):
@@ -177,7 +185,8 @@ def _upload(comm, args: list, ranks: list, out_bytes: int):
     for a, r in zip(args, ranks):
         dst = io.tensor(r, 0, a.nbytes)
         if a.nbytes:
-            dst.copy_(a.t.view(torch.uint8).reshape(-1), non_blocking=False)
+            src = a.t.view(torch.uint8).reshape(-1)
+            dst.copy_(src, non_blocking=src.is_pinned())
         sends.append(dst.view(a.t.dtype))
         recvs.append(io.tensor(r, _align(in_bytes), out_bytes).view(a.t.dtype))
     return sends, recvs
@@ -215,13 +224,16 @@ def _run(comm, buf, reduce: bool, algo: str, order: str, out=None):
             _reduce_scatter_device(comm, algo, order, sends, recvs, emu)
         else:
             _all_gather_device(comm, algo, sends, recvs, emu)
-        if emu or any(a.host for a in args):
+        host = _download([rv for a, rv in zip(args, recvs) if a.host])
+        if emu and not host:
             torch.cuda.current_stream(comm.device).synchronize()
+        if emu or host:
             comm.world.check()
-        res = []
+        res, hi = [], 0
         for a, rv in zip(args, recvs):
             if a.host:
-                res.append(_finish(a, rv))
+                res.append(_finish(a, host[hi]))
+                hi += 1
             else:
                 res.append(rv if a.out is None else a.out)
         return res

@@ -8,14 +8,15 @@
 //     its own memory (ld.acquire.sys), the writer publishes with st.release.sys
 //     after a CTA barrier — one NVLink write per signal, no remote polling;
 //   * READY[src][cta] carries a monotonic progress counter
-//     (epoch << 20 | units_done) so flags are never reset between calls: the
+//     (epoch << 32 | hash << 10 | units_done) so flags are never reset: the
 //     per-group epoch plays the role of next_base_tag()'s sequence number
 //     (transport/base.py:131-138);
 //   * DONE[src][cta] = epoch once src has finished reading this rank's buffers
 //     (the WAR guard that lets the caller reuse them after the call);
-//   * META[src][cta] = epoch << 32 | call-signature hash, checked on first
-//     contact: a cross-rank size/dtype/algorithm mismatch raises
-//     LengthMismatch like from_payload (collectives.py:36-42);
+//   * the READY word also carries 22 bits of the call-signature hash
+//     (count, dtype, algorithm, variant, placement), checked on every wait: a
+//     cross-rank mismatch raises LengthMismatch like from_payload
+//     (collectives.py:36-42);
 //   * a wait that sees ABORT_BIT, or exceeds the %globaltimer deadline, records
 //     the error in the world's host-mapped error word and floods ABORT into
 //     every member's slot so no CTA on any GPU is left spinning.
@@ -28,7 +29,7 @@
 #ifndef PCCL_MAXR
 #define PCCL_MAXR 16
 #endif
-#define PCCL_MAX_CTAS 160
+#define PCCL_MAX_CTAS 320
 #define PCCL_NSLOTS 256
 #define PCCL_SLOT_WORDS (3 * PCCL_MAXR * PCCL_MAX_CTAS)
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
@@ -77,7 +78,11 @@ struct LaunchParams {
   char *work[PCCL_MAXR];
   char *out[PCCL_MAXR];
   volatile int *err;                  // host-mapped error word
+  uint64_t *trace;                    // optional: per (row, cta) event log, PCCL_TRACE_EVENTS words
 };
+
+#define PCCL_TRACE_EVENTS 128
+enum TraceKind { TR_START = 1, TR_WAIT = 2, TR_SIGNAL = 3, TR_END = 4 };
 
 // --------------------------------------------------------------------------
 // memory-model primitives
@@ -109,6 +114,8 @@ struct Ctx {
   uint64_t epoch;
   uint64_t *my_slot;
   uint64_t t0;
+  uint64_t *tr;  // trace cursor base (nullptr: tracing off)
+  int ntr;
 
   __device__ __forceinline__ int world(int m) const { return P->gmem[y][m]; }
   __device__ __forceinline__ uint64_t *slot_in(int m) const {
@@ -130,7 +137,16 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.epoch = P.epoch[c.y];
   c.my_slot = P.flags[c.r] + P.slot_off[c.y];
   c.t0 = global_timer_ns();
+  c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
+  c.ntr = 0;
+  if (c.tr && threadIdx.x == 0) c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
   return c;
+}
+
+// thread 0 only: append (time, kind, unit) to this CTA's trace
+__device__ __forceinline__ void trace_ev(Ctx &c, int kind, int unit) {
+  if (c.tr && threadIdx.x == 0 && c.ntr < PCCL_TRACE_EVENTS)
+    c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)kind << 12) | (uint64_t)(unit & 0xfff);
 }
 
 // Flood ABORT into every member's slot (all sources, all CTAs) so that every
@@ -171,22 +187,40 @@ __host__ __device__ __forceinline__ int recdbl_partner(int gi, int k) { return g
 // recursive halving RS, step k (collectives.py:151-153)
 __host__ __device__ __forceinline__ int rechalf_partner(int gi, int gs, int k) { return gi ^ (gs >> (k + 1)); }
 
-__device__ __forceinline__ uint64_t ready_value(uint64_t epoch, int unit) {
-  return (epoch << 20) | (uint64_t)(unit + 1);
+// READY word: epoch << 32 | (call-signature hash & 0x3fffff) << 10 | (unit + 1).
+// Folding the signature into the progress word makes the cross-rank check
+// free: no separate META store (and no extra fence) on the entry handshake.
+__device__ __forceinline__ uint64_t ready_value(const Ctx &c, int unit) {
+  return (c.epoch << 32) | ((uint64_t)(c.P->meta[c.y] & 0x3fffffu) << 10) | (uint64_t)(unit + 1);
 }
-
-// CTA-wide: wait until member m has completed `unit`; optionally verify its
-// call signature. Returns false (after aborting the group) on error.
-__device__ __forceinline__ bool cta_wait(const Ctx &c, int m, int unit, bool check_meta) {
-  int code = 0;
-  if (threadIdx.x == 0) {
-    code = spin_ge(c, Ctx::word(c.my_slot, F_READY, m, c.b), ready_value(c.epoch, unit));
-    if (code == 0 && check_meta) {
-      uint64_t got = ld_acquire_sys(Ctx::word(c.my_slot, F_META, m, c.b));
-      uint64_t want = (c.epoch << 32) | c.P->meta[c.y];
-      if (got != want) code = 4;  // PCCL_ERR_LENGTH_MISMATCH
+// 0 = satisfied, > 0 = error code, -1 = not yet. A later epoch satisfies any
+// wait of an earlier one (the writer already published everything of ours).
+__device__ __forceinline__ int ready_check(const Ctx &c, uint64_t v, int unit) {
+  if (v & PCCL_ABORT_BIT) return (int)(v & 0xff);
+  const uint64_t ep = (v >> 32) & 0x7fffffffull;
+  if (ep > c.epoch) return 0;
+  if (ep < c.epoch) return -1;
+  if (((v >> 10) & 0x3fffffu) != (c.P->meta[c.y] & 0x3fffffu)) return 4;  // PCCL_ERR_LENGTH_MISMATCH
+  return (v & 0x3ffu) >= (uint64_t)(unit + 1) ? 0 : -1;
+}
+__device__ __forceinline__ int spin_ready(const Ctx &c, const uint64_t *w, int unit) {
+  uint32_t it = 0;
+  while (true) {
+    const int r = ready_check(c, ld_acquire_sys(w), unit);
+    if (r >= 0) return r;
+    if ((++it & 255u) == 0) {
+      if (*c.P->err != 0) return *c.P->err;
+      if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;  // PCCL_ERR_TIMEOUT
     }
   }
+}
+
+// CTA-wide: wait until member m has completed `unit` (its call signature is
+// verified on every wait). Returns false (after aborting the group) on error.
+__device__ __forceinline__ bool cta_wait(Ctx &c, int m, int unit, bool check_meta = true) {
+  (void)check_meta;
+  int code = 0;
+  if (threadIdx.x == 0) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, c.b), unit);
   int ok = __syncthreads_and(code == 0);
   if (!ok) {
     __shared__ int s_code;
@@ -195,20 +229,16 @@ __device__ __forceinline__ bool cta_wait(const Ctx &c, int m, int unit, bool che
     if (s_code != 0) abort_group(c, s_code);
     return false;
   }
+  trace_ev(c, TR_WAIT, unit);
   return true;
 }
 
 // CTA-wide: wait for every member in `mask` (bit m) to complete `unit`.
-__device__ __forceinline__ bool cta_wait_mask(const Ctx &c, uint32_t mask, int unit, bool check_meta) {
+__device__ __forceinline__ bool cta_wait_mask(Ctx &c, uint32_t mask, int unit, bool check_meta = true) {
+  (void)check_meta;
   int code = 0;
   const int m = threadIdx.x;
-  if (m < c.gs && ((mask >> m) & 1u)) {
-    code = spin_ge(c, Ctx::word(c.my_slot, F_READY, m, c.b), ready_value(c.epoch, unit));
-    if (code == 0 && check_meta) {
-      uint64_t got = ld_acquire_sys(Ctx::word(c.my_slot, F_META, m, c.b));
-      if (got != ((c.epoch << 32) | c.P->meta[c.y])) code = 4;
-    }
-  }
+  if (m < c.gs && ((mask >> m) & 1u)) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, c.b), unit);
   int ok = __syncthreads_and(code == 0);
   if (!ok) {
     __shared__ int s_code;
@@ -219,32 +249,30 @@ __device__ __forceinline__ bool cta_wait_mask(const Ctx &c, uint32_t mask, int u
     abort_group(c, s_code ? s_code : 5);
     return false;
   }
+  trace_ev(c, TR_WAIT, unit);
   return true;
 }
 
 // CTA-wide: publish completion of `unit` to member m (after a CTA barrier so
 // every thread's stores of the unit are ordered before the release).
-__device__ __forceinline__ void cta_signal(const Ctx &c, int m, int unit) {
+__device__ __forceinline__ void cta_signal(Ctx &c, int m, int unit) {
   __syncthreads();
-  if (threadIdx.x == 0) st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c.epoch, unit));
+  if (threadIdx.x == 0) st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
+  trace_ev(c, TR_SIGNAL, unit);
 }
-__device__ __forceinline__ void cta_signal_mask(const Ctx &c, uint32_t mask, int unit) {
+__device__ __forceinline__ void cta_signal_mask(Ctx &c, uint32_t mask, int unit) {
   __syncthreads();
   const int m = threadIdx.x;
   if (m < c.gs && ((mask >> m) & 1u))
-    st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c.epoch, unit));
+    st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
+  trace_ev(c, TR_SIGNAL, unit);
 }
-// Write this call's signature into every member in mask (ordered before the
-// first READY release to that member by that release).
-__device__ __forceinline__ void cta_publish_meta(const Ctx &c, uint32_t mask) {
-  const int m = threadIdx.x;
-  if (m < c.gs && ((mask >> m) & 1u))
-    st_relaxed_sys(Ctx::word(c.slot_in(m), F_META, c.gi, c.b), (c.epoch << 32) | c.P->meta[c.y]);
-}
+// Kept for call-site symmetry: the signature now travels in the READY word.
+__device__ __forceinline__ void cta_publish_meta(const Ctx &, uint32_t) {}
 
 // Exit barrier: tell every member in `to` that this CTA has finished reading
 // their buffers; wait until every member in `from` has finished reading ours.
-__device__ __forceinline__ bool cta_exit(const Ctx &c, uint32_t to, uint32_t from) {
+__device__ __forceinline__ bool cta_exit(Ctx &c, uint32_t to, uint32_t from) {
   if (c.P->skip_exit) return true;
   __syncthreads();
   const int m = threadIdx.x;
@@ -261,6 +289,7 @@ __device__ __forceinline__ bool cta_exit(const Ctx &c, uint32_t to, uint32_t fro
     abort_group(c, s_code ? s_code : 5);
     return false;
   }
+  trace_ev(c, TR_END, 0);
   return true;
 }
 

@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   cta_signal_mask(c, peers, 0);  // my recv may be written
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  if (P.local_copy) ag_local_copy<U>(c, lo, hi);
   if (!cta_wait_mask(c, peers, 0, true)) return;
   for (int i = 1; i < c.gs; ++i) {
     const int q = (c.gi + i) % c.gs;
@@ -166,6 +165,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
       store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
   }
   cta_signal_mask(c, peers, 1);  // my block has landed in your recv
+  if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
   if (!cta_wait_mask(c, peers, 1, false)) return;
 }
 
@@ -306,6 +306,200 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
   cta_exit(c, partners, partners);
 }
 
+
+// ============================================================================
+// PUSH family (ag_variant / rs_variant 1). Data moves as posted NVLink stores
+// into the consumer's symmetric buffer; the consumer only reads local HBM.
+// Channel protocol per (writer -> reader) pair: unit 0 travels reader ->
+// writer ("my receive buffer is free": the reader's kernel for this call has
+// started, so nothing of the previous call still reads it), data units
+// 1 + step*nsub + t travel writer -> reader after the stores of that
+// sub-slice (release after a CTA barrier). No exit barrier is needed: a
+// writer only reads its own buffers.
+// ============================================================================
+__device__ __forceinline__ int push_unit(int step, int nsub, int t) { return 1 + step * nsub + t; }
+
+// AG ring, push: step s forwards block (gi - s) to next's recv.
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub;
+  const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
+  cta_publish_meta(c, (1u << next) | (1u << prev));
+  cta_signal(c, prev, 0);  // my recv is free
+  if (!cta_wait(c, next, 0, true)) return;
+  char *my = P.recv[c.r];
+  char *nx = P.recv[c.world(next)];
+  for (int s = 0; s < gs - 1; ++s) {
+    const int blk = (c.gi - s + gs) % gs;
+    for (int t = 0; t < nsub; ++t) {
+      if (s > 0 && !cta_wait(c, prev, push_unit(s - 1, nsub, t), s == 1 && t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int j = 0; j < P.nsubblk; ++j) {
+        const char *src = (s == 0) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U : ag_block<U>(P, my, c.y, blk, j);
+        copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), src, lo, hi);
+      }
+      cta_signal(c, next, push_unit(s, nsub, t));
+    }
+  }
+  for (int t = 0; t < nsub; ++t)
+    if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t), gs == 2 && t == 0)) return;
+  if (P.local_copy) {
+    int64_t lo, hi;
+    split32(P.blk, P.ctas, c.b, lo, hi);
+    ag_local_copy<U>(c, lo, hi);
+  }
+}
+
+// AG recursive doubling, push: step k sends my 2^k gathered blocks to r ^ 2^k.
+template <int U>
+__global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
+  uint32_t partners = 0;
+  for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
+  cta_publish_meta(c, partners);
+  cta_signal_mask(c, partners, 0);  // my recv is free
+  char *my = P.recv[c.r];
+  for (int k = 0; k < L; ++k) {
+    const int partner = recdbl_partner(c.gi, k);
+    if (!cta_wait(c, partner, 0, true)) return;
+    char *pr = P.recv[c.world(partner)];
+    const int start = (c.gi >> k) << k, width = 1 << k;
+    for (int t = 0; t < nsub; ++t) {
+      if (k > 0 && !cta_wait(c, recdbl_partner(c.gi, k - 1), push_unit(k - 1, nsub, t), false)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int i = start; i < start + width; ++i)
+        for (int j = 0; j < P.nsubblk; ++j) {
+          const char *src = (i == c.gi) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U : ag_block<U>(P, my, c.y, i, j);
+          copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), src, lo, hi);
+        }
+      cta_signal(c, partner, push_unit(k, nsub, t));
+    }
+  }
+  for (int t = 0; t < nsub; ++t)
+    if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t), false)) return;
+  if (P.local_copy) {
+    int64_t lo, hi;
+    split32(P.blk, P.ctas, c.b, lo, hi);
+    ag_local_copy<U>(c, lo, hi);
+  }
+}
+
+// RS ring, push with the add at the sender: v = own chunk + carry received in
+// my staging, stored into next's staging (or my output on the last step).
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rs_ring_push(const __grid_constant__ LaunchParams P) {
+  using T = typename RUnit<DT, VEC>::T;
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub;
+  const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
+  cta_publish_meta(c, (1u << next) | (1u << prev));
+  cta_signal(c, prev, 0);  // my staging is free
+  if (!cta_wait(c, next, 0, true)) return;
+  char *sendp = P.send[c.r], *stg = P.recv[c.r], *nstg = P.recv[c.world(next)], *outp = P.out[c.r];
+  {
+    const int ch = (c.gi - 1 + gs) % gs;  // initial carry (collectives.py:98)
+    for (int t = 0; t < nsub; ++t) {
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int j = 0; j < P.nsubblk; ++j)
+        copy_units<(int)sizeof(T), kUnroll>(rs_chunk<T>(P, nstg, c.y, ch, j), rs_chunk<T>(P, sendp, c.y, ch, j), lo, hi);
+      cta_signal(c, next, push_unit(0, nsub, t));
+    }
+  }
+  for (int s = 1; s < gs; ++s) {
+    const int ch = ((c.gi - s - 1) % gs + gs) % gs;
+    const bool last = (s == gs - 1);
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, prev, push_unit(s - 1, nsub, t), s == 1 && t == 0)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int j = 0; j < P.nsubblk; ++j) {
+        char *dst = last ? outp + (int64_t)j * P.out_sub_stride * (int64_t)sizeof(T) : rs_chunk<T>(P, nstg, c.y, ch, j);
+        reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, sendp, c.y, ch, j), rs_chunk<T>(P, stg, c.y, ch, j), lo, hi);
+      }
+      if (!last) cta_signal(c, next, push_unit(s, nsub, t));
+    }
+  }
+}
+
+// RS recursive halving, push with the add at the sender. Staging region k
+// (chunks [gs - gs/2^k, ...)) receives partner_k's partial over mine_k; the
+// result of step k is written locally for mine_{k+1} and straight into
+// partner_{k+1}'s staging region k+1 for theirs_{k+1}.
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant__ LaunchParams P) {
+  using T = typename RUnit<DT, VEC>::T;
+  Ctx c = make_ctx(P);
+  const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
+  uint32_t partners = 0;
+  for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
+  cta_publish_meta(c, partners);
+  cta_signal_mask(c, partners, 0);  // my staging is free
+  char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r], *stgp = P.recv[c.r];
+  // staging slot of absolute chunk ch received at step k (region base = gs - gs/2^k chunks)
+  auto stg_chunk = [&](char *buf, int k, int lo_k, int ch, int j) -> char * {
+    const int slot = (gs - (gs >> k)) + (ch - lo_k);
+    return rs_chunk<T>(P, buf, c.y, slot, j);
+  };
+  // step "-1": raw input over theirs_0 into partner_0's staging region 0
+  {
+    const int partner = rechalf_partner(c.gi, gs, 0);
+    if (!cta_wait(c, partner, 0, true)) return;
+    const int half = gs / 2, mid = half;
+    const int t0 = c.gi < mid ? mid : 0, t1 = c.gi < mid ? gs : mid;  // theirs_0
+    char *pst = P.recv[c.world(partner)];
+    for (int t = 0; t < nsub; ++t) {
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int ch = t0; ch < t1; ++ch)
+        for (int j = 0; j < P.nsubblk; ++j)
+          copy_units<(int)sizeof(T), kUnroll>(stg_chunk(pst, 0, t0, ch, j), rs_chunk<T>(P, sendp, c.y, ch, j), lo, hi);
+      cta_signal(c, partner, push_unit(0, nsub, t));
+    }
+  }
+  int lo_c = 0, hi_c = gs;
+  for (int k = 0; k < L; ++k) {
+    const int half = (hi_c - lo_c) / 2, mid = lo_c + half;
+    const int partner = c.gi ^ half;  // == rechalf_partner(c.gi, gs, k)
+    int m0, m1;
+    if (c.gi < mid) { m0 = lo_c; m1 = mid; } else { m0 = mid; m1 = hi_c; }
+    const bool last = (k == L - 1);
+    // next step's split of mine_k
+    int n0 = m0, n1 = m1, nxt = -1;
+    char *nst = nullptr;
+    if (!last) {
+      const int h2 = (m1 - m0) / 2, mid2 = m0 + h2;
+      if (c.gi < mid2) { n0 = m0; n1 = mid2; } else { n0 = mid2; n1 = m1; }
+      nxt = c.gi ^ h2;
+      if (!cta_wait(c, nxt, 0, false)) return;
+      nst = P.recv[c.world(nxt)];
+    }
+    const int t_lo = (n0 == m0) ? n1 : m0;  // theirs_{k+1} = mine_k \ mine_{k+1}
+    const char *local = (k == 0) ? sendp : workp;
+    for (int t = 0; t < nsub; ++t) {
+      if (!cta_wait(c, partner, push_unit(k, nsub, t), false)) return;
+      int64_t lo, hi;
+      cta_subslice(c, t, lo, hi);
+      for (int ch = m0; ch < m1; ++ch)
+        for (int j = 0; j < P.nsubblk; ++j) {
+          char *dst;
+          if (last) dst = outp + (int64_t)j * P.out_sub_stride * (int64_t)sizeof(T);
+          else if (ch >= n0 && ch < n1) dst = rs_chunk<T>(P, workp, c.y, ch, j);
+          else dst = stg_chunk(nst, k + 1, t_lo, ch, j);
+          reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, const_cast<char *>(local), c.y, ch, j),
+                                          stg_chunk(stgp, k, m0, ch, j), lo, hi);
+        }
+      if (!last) cta_signal(c, nxt, push_unit(k + 1, nsub, t));
+    }
+    lo_c = m0;
+    hi_c = m1;
+  }
+}
+
 // Direct reduce-scatter, one step. PULL: every member's chunk `gi` is read
 // from the peers' symmetric send buffers. PUSH: every rank first stores its
 // chunk q into member q's staging slot [gi] (posted NVLink writes), then folds
@@ -343,7 +537,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   if (PUSH) {
     for (int i = 1; i < gs; ++i) {
       const int q = (gi + i) % gs;
-      T *dst = reinterpret_cast<T *>(P.work[c.world(q)]) + (int64_t)gi * P.blk;
+      T *dst = reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk;
       copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
     }
     cta_signal_mask(c, peers, 1);  // my chunks have landed
@@ -359,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
     if (i >= gs) q = gi;
     if (PUSH)
       src[i] = (q == gi) ? own + P.base[c.y] + (int64_t)gi * P.istride
-                         : reinterpret_cast<const T *>(P.work[c.r]) + (int64_t)q * P.blk;
+                         : reinterpret_cast<const T *>(P.recv[c.r]) + (int64_t)q * P.blk;
     else
       src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]) + P.base[c.y] + (int64_t)gi * P.istride;
   }

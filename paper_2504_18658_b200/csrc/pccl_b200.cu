@@ -43,11 +43,15 @@ struct pccl_world {
   // tuning knobs (pccl_world_set_param)
   int64_t p_ctas = 0;  // 0: auto
   int64_t p_nsub = 1;
-  int64_t p_ag_variant = 0;
-  int64_t p_rs_variant = 0;
+  int64_t p_threads = 512;
+  int64_t p_ag_variant = -1;  // -1: auto (per algorithm / buffer registration)
+  int64_t p_rs_variant = -1;
   int64_t p_tma_stages = 3;
   int64_t p_tma_tile = 65536;
   int64_t p_timeout_ms = 20000;
+  int64_t p_trace = 0;
+  uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
+  int trace_rows = 0, trace_ctas = 0;
   uint32_t meta_skew[PCCL_MAXR] = {};
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
 };
@@ -172,8 +176,8 @@ KernelFn rs_direct_kernel(int order, int maxp) {
 
 template <int DT, bool VEC>
 KernelFn rs_kernel_dt(int algo, int order, int maxp, int variant) {
-  if (algo == A_RING) return (KernelFn)k_rs_ring<DT, VEC>;
-  if (algo == A_REC) return (KernelFn)k_rs_rec<DT, VEC>;
+  if (algo == A_RING) return variant == 1 ? (KernelFn)k_rs_ring_push<DT, VEC> : (KernelFn)k_rs_ring<DT, VEC>;
+  if (algo == A_REC) return variant == 1 ? (KernelFn)k_rs_rec_push<DT, VEC> : (KernelFn)k_rs_rec<DT, VEC>;
   return variant == 1 ? rs_direct_kernel<DT, VEC, true>(order, maxp) : rs_direct_kernel<DT, VEC, false>(order, maxp);
 }
 
@@ -224,7 +228,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.order = pl.order;
   P.timeout_ns = (w->p_timeout_ms * 1000000ll);
   P.err = w->err_dev;
-  P.nsub = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_nsub, 64));
+  P.nsub = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_nsub, 32));
   P.variant = pl.variant;
   P.tma_stages = (int)w->p_tma_stages;
   P.tma_tile = (uint32_t)w->p_tma_tile;
@@ -249,6 +253,24 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     while (U > 1 && (acc & (uint64_t)(U - 1))) U >>= 1;
     if ((size_t)U < es && es <= 16 && !(acc & (es - 1))) U = (int)es;
     k = ag_kernel(pl.algo, U);
+    if (pl.variant == 1 && pl.algo == A_RING) {
+      switch (U) {
+        case 16: k = (KernelFn)k_ag_ring_push<16>; break;
+        case 8: k = (KernelFn)k_ag_ring_push<8>; break;
+        case 4: k = (KernelFn)k_ag_ring_push<4>; break;
+        case 2: k = (KernelFn)k_ag_ring_push<2>; break;
+        default: k = (KernelFn)k_ag_ring_push<1>; break;
+      }
+    }
+    if (pl.variant == 1 && pl.algo == A_REC) {
+      switch (U) {
+        case 16: k = (KernelFn)k_ag_rec_push<16>; break;
+        case 8: k = (KernelFn)k_ag_rec_push<8>; break;
+        case 4: k = (KernelFn)k_ag_rec_push<4>; break;
+        case 2: k = (KernelFn)k_ag_rec_push<2>; break;
+        default: k = (KernelFn)k_ag_rec_push<1>; break;
+      }
+    }
     if (pl.algo == A_DIRECT && (pl.variant == 1 || pl.variant == 3))
       k = U == 16 ? (KernelFn)k_ag_direct_push<16> : (KernelFn)k_ag_direct_push<1>;
     if (pl.algo == A_DIRECT && (pl.variant == 1 || pl.variant == 3) && U != 16) {
@@ -297,7 +319,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     auto it = slot_epoch.find(g->slot);
     if (it == slot_epoch.end()) it = slot_epoch.emplace(g->slot, ++w->epoch[g->slot]).first;
     P.epoch[y] = it->second;
-    P.meta[y] = (hash_meta(pl.coll, pl.algo, pl.order, pl.count, pl.dtype, pl.gs) ^ (pl.place * 2654435761u) ^
+    P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order, pl.count, pl.dtype, pl.gs) ^ (pl.place * 2654435761u) ^
                  w->meta_skew[rw.rank]) & 0x7fffffffu;
   }
   for (int q = 0; q < w->nranks; ++q) {
@@ -309,8 +331,14 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   }
 
   // ---- grid
-  const int threads = kThreads;
-  int ctas = w->p_ctas > 0 ? (int)w->p_ctas : (w->emu ? PCCL_MAX_CTAS : 128);
+  const int threads = (int)std::max<int64_t>(64, std::min<int64_t>(w->p_threads, kThreads));
+  int ctas = (int)w->p_ctas;
+  if (ctas <= 0) {
+    // auto (measured, tools/sweep.py at p=4): latency-bound small messages
+    // want few CTAs (fewer flags), >= 32 MiB wants ~one CTA per SM.
+    const double S = (double)pl.gs * (double)pl.count * (double)es;
+    ctas = w->emu ? PCCL_MAX_CTAS : (S >= 32.0 * (1 << 20) ? 128 : S >= 4.0 * (1 << 20) ? 64 : S >= 2.0 * (1 << 20) ? 32 : 16);
+  }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
   {
     int per_sm = 0;
@@ -320,6 +348,14 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     ctas = std::max(1, std::min(ctas, cap / nrows));
   }
   P.ctas = ctas;
+  if (w->p_trace) {
+    const size_t words = (size_t)PCCL_MAXR * PCCL_MAX_CTAS * PCCL_TRACE_EVENTS;
+    if (!w->trace_buf) CK(cudaMalloc((void **)&w->trace_buf, words * 8));
+    CK(cudaMemsetAsync(w->trace_buf, 0, (size_t)nrows * ctas * PCCL_TRACE_EVENTS * 8, stream));
+    P.trace = w->trace_buf;
+    w->trace_rows = nrows;
+    w->trace_ctas = ctas;
+  }
   dim3 grid(ctas, nrows), block(threads);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (w->emu) {
@@ -436,7 +472,20 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.blk = (int64_t)count;
   pl.istride = (int64_t)count;
   pl.send_sub_stride = (int64_t)count;
-  pl.variant = algo == A_DIRECT ? (int)w->p_ag_variant : 0;
+  {
+    // Data movement. auto: push (posted NVLink stores, saturates the links
+    // with few SMs) whenever the output is symmetric; a direct all-gather into
+    // an unregistered output pulls instead (only the small send is staged).
+    int v = (int)w->p_ag_variant;
+    if (v < 0) {
+      int seg;
+      size_t off;
+      const bool recv_reg = resolve(w, ranks[0], recvs[0], gs * blk_bytes, &seg, &off);
+      v = (recv_reg || algo != A_DIRECT) ? 1 : 0;
+    }
+    if (algo != A_DIRECT && v != 1) v = 0;  // TMA variants exist for direct only
+    pl.variant = v;
+  }
   Binder B{w, stream};
   std::vector<std::pair<char *, char *>> copy_out;  // (staged recv, user recv)
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -502,7 +551,19 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.blk = (int64_t)recvcount;
   pl.istride = (int64_t)recvcount;
   pl.out_sub_stride = (int64_t)recvcount;
-  pl.variant = algo == A_DIRECT ? (int)w->p_rs_variant : 0;
+  {
+    // auto: pull (peer loads fused with the add, no staging hop) for direct /
+    // recursive halving when the input is symmetric; push for ring, and for
+    // every algorithm when the input is unregistered (no input staging copy).
+    int v = (int)w->p_rs_variant;
+    if (v < 0) {
+      int seg;
+      size_t off;
+      const bool send_reg = resolve(w, ranks[0], sends[0], gs * chunk_bytes, &seg, &off);
+      v = (!send_reg || algo == A_RING) ? 1 : 0;
+    }
+    pl.variant = v == 1 ? 1 : 0;
+  }
   Binder B{w, stream};
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
@@ -512,9 +573,10 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     pl.rows.push_back({r, c});
     B.cursor = 0;
     if (pl.variant == 1) {
-      // push: send is read locally only; peers write into my staging slots
+      // push: send is read locally only; peers write into my staging (recv)
       pl.send[r] = (char *)sends[i];
-      if (!B.scratch(r, gs * chunk_bytes, pl.work)) return B.status;
+      if (!B.scratch(r, gs * chunk_bytes, pl.recv)) return B.status;
+      if (algo == A_REC && !B.scratch(r, gs * chunk_bytes, pl.work)) return B.status;
       pl.out[r] = (char *)recvs[i];
       continue;
     }
@@ -736,6 +798,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_TIMEOUT_MS")) w->p_timeout_ms = atoll(t);
   if (const char *t = getenv("PCCL_CTAS")) w->p_ctas = atoi(t);
   if (const char *t = getenv("PCCL_NSUB")) w->p_nsub = atoi(t);
+  if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
   if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
   if (const char *t = getenv("PCCL_TMA_STAGES")) w->p_tma_stages = atoi(t);
@@ -775,6 +838,7 @@ int pccl_world_destroy(pccl_world_t w) {
   for (int s = kMaxSegs - 1; s >= 0; --s)
     if (w->segs[s].used) pccl_segment_destroy(w, s);
   if (w->err_host) cudaFreeHost((void *)w->err_host);
+  if (w->trace_buf) cudaFree(w->trace_buf);
   delete w;
   return PCCL_SUCCESS;
 }
@@ -797,7 +861,7 @@ int pccl_world_reset_flags(pccl_world_t w) {
 }
 
 int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads) {
-  if (!w || ctas < 0 || ctas > PCCL_MAX_CTAS || nsub < 0 || nsub > 64) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!w || ctas < 0 || ctas > PCCL_MAX_CTAS || nsub < 0 || nsub > 32) return PCCL_ERR_INVALID_ARGUMENT;
   w->p_ctas = ctas;
   if (nsub) w->p_nsub = nsub;
   (void)threads;
@@ -813,20 +877,24 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms) {
 static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "ctas")) return &w->p_ctas;
   if (!strcmp(key, "nsub")) return &w->p_nsub;
+  if (!strcmp(key, "threads")) return &w->p_threads;
   if (!strcmp(key, "ag_variant")) return &w->p_ag_variant;
   if (!strcmp(key, "rs_variant")) return &w->p_rs_variant;
   if (!strcmp(key, "tma_stages")) return &w->p_tma_stages;
   if (!strcmp(key, "tma_tile")) return &w->p_tma_tile;
   if (!strcmp(key, "timeout_ms")) return &w->p_timeout_ms;
+  if (!strcmp(key, "trace")) return &w->p_trace;
   return nullptr;
 }
 
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!w || !key) return PCCL_ERR_INVALID_ARGUMENT;
   int64_t *ref = param_ref(w, key);
-  if (!ref || value < 0) return PCCL_ERR_INVALID_ARGUMENT;
+  const bool is_variant = !strcmp(key, "ag_variant") || !strcmp(key, "rs_variant");
+  if (!ref || value < (is_variant ? -1 : 0)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
-  if (!strcmp(key, "nsub") && (value < 1 || value > 64)) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if ((!strcmp(key, "ag_variant") || !strcmp(key, "rs_variant")) && value > 3) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
@@ -840,6 +908,19 @@ int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value) {
   int64_t *ref = param_ref(w, key);
   if (!ref) return PCCL_ERR_INVALID_ARGUMENT;
   *value = *ref;
+  return PCCL_SUCCESS;
+}
+
+int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas) {
+  if (!w || !host || !rows || !ctas) return PCCL_ERR_INVALID_ARGUMENT;
+  *rows = w->trace_rows;
+  *ctas = w->trace_ctas;
+  if (!w->trace_buf) return PCCL_SUCCESS;
+  const size_t words = (size_t)w->trace_rows * w->trace_ctas * PCCL_TRACE_EVENTS;
+  if (cap_words < words) return PCCL_ERR_OUT_OF_MEMORY;
+  CK(cudaSetDevice(w->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host, w->trace_buf, words * 8, cudaMemcpyDeviceToHost));
   return PCCL_SUCCESS;
 }
 

@@ -24,6 +24,7 @@ from .collectives import (
     _In,
     _align,
     _ensure_io,
+    _download,
     _finish,
     _stream,
     as_elements,
@@ -177,7 +178,8 @@ def _hier(plan: HierPlan, comm, buf, reduce: bool, out=None):
             for a, r in zip(args, ranks):
                 dst = io.tensor(r, 0, a.nbytes)
                 if a.nbytes:
-                    dst.copy_(a.t.view(torch.uint8).reshape(-1))
+                    src = a.t.view(torch.uint8).reshape(-1)
+                    dst.copy_(src, non_blocking=src.is_pinned())
                 sends.append(dst.view(a.t.dtype))
                 recvs.append(io.tensor(r, _align(in_bytes), out_numel * es).view(a.t.dtype))
         else:
@@ -193,10 +195,19 @@ def _hier(plan: HierPlan, comm, buf, reduce: bool, out=None):
             fn = lib().pccl_hier_reduce_scatter if reduce else lib().pccl_hier_all_gather
             st = fn(world.handle, N, M, inter, sends[0].data_ptr(), recvs[0].data_ptr(), n, dtype, stream)
         check(st, "hier_reduce_scatter" if reduce else "hier_all_gather")
-        if emu or any(a.host for a in args):
+        host = _download([rv for a, rv in zip(args, recvs) if a.host])
+        if emu and not host:
             torch.cuda.current_stream(comm.device).synchronize()
+        if emu or host:
             world.check()
-        return [_finish(a, rv) if a.host else (rv if a.out is None else a.out) for a, rv in zip(args, recvs)]
+        res, hi = [], 0
+        for a, rv in zip(args, recvs):
+            if a.host:
+                res.append(_finish(a, host[hi]))
+                hi += 1
+            else:
+                res.append(rv if a.out is None else a.out)
+        return res
 
     if comm.emulated:
         return comm._rendezvous(arg, execute)

@@ -188,6 +188,24 @@ class World:
         check(lib().pccl_world_get_param(self.handle, key.encode(), ctypes.byref(v)), f"get_param({key})")
         return v.value
 
+    def trace(self):
+        """Events of the last launch (param "trace" = 1): list over rows of
+        lists over CTAs of (t_ns, kind, unit) tuples; kinds: 1 start, 2 wait
+        done, 3 signal, 4 end."""
+        cap = 16 * 320 * 128
+        buf = (ctypes.c_uint64 * cap)()
+        rows, ctas = ctypes.c_int(), ctypes.c_int()
+        check(lib().pccl_world_trace(self.handle, buf, cap, ctypes.byref(rows), ctypes.byref(ctas)), "trace")
+        out = []
+        for y in range(rows.value):
+            row = []
+            for b in range(ctas.value):
+                base = (y * ctas.value + b) * 128
+                ev = [(int(v) >> 16, (int(v) >> 12) & 0xF, int(v) & 0xFFF) for v in buf[base:base + 128] if v]
+                row.append(ev)
+            out.append(row)
+        return out
+
     def set_timeout_ms(self, ms: int) -> None:
         check(lib().pccl_world_set_timeout_ms(self.handle, ms), "set_timeout")
 

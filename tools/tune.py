@@ -17,11 +17,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size-mib", type=int, default=128)
     ap.add_argument("--ctas", default="16,32,64,96,128")
-    ap.add_argument("--nsub", default="1,4")
+    ap.add_argument("--nsub", default="1")
+    ap.add_argument("--threads", default="512")
     ap.add_argument("--colls", default="ag_f32,rs_bf16")
     ap.add_argument("--algos", default="direct,ring,recursive")
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--variants", default="0")
+    ap.add_argument("--variants", default="-1")
     ap.add_argument("--tma", default="4x32768", help="stages x tile bytes list, comma separated")
     args = ap.parse_args()
     rank = int(os.environ["RANK"])
@@ -58,7 +59,7 @@ def main():
             world.ensure_staging(int(L.pccl_staging_bytes(0 if kind == "ag" else 1, a, p, n, code)))
             combos = []
             for v in map(int, args.variants.split(",")):
-                if v and algo != "direct":
+                if v >= 2 and algo != "direct":
                     continue
                 if v >= 2 and kind == "rs":
                     continue
@@ -69,7 +70,8 @@ def main():
               if stg:
                   world.set_param("tma_stages", stg)
                   world.set_param("tma_tile", tile)
-              for ctas in map(int, args.ctas.split(",")):
+              for thr, ctas in [(th, ct) for th in map(int, args.threads.split(",")) for ct in map(int, args.ctas.split(","))]:
+                world.set_param("threads", thr)
                 for nsub in map(int, args.nsub.split(",")):
                     world.set_tuning(ctas, nsub)
                     if kind == "ag":
@@ -95,13 +97,13 @@ def main():
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     us = float(t) * 1e3
                     bw = S * (p - 1) / p / (us * 1e-6) / 1e9
-                    results.append(dict(coll=coll, algo=algo, variant=variant, stages=stg, tile=tile, ctas=ctas,
+                    results.append(dict(coll=coll, algo=algo, variant=variant, stages=stg, tile=tile, ctas=ctas, threads=thr,
                                         nsub=nsub, us=round(us, 1), busbw=round(bw, 1)))
                     if rank == 0:
-                        print(f"p={p} {coll:8s} {algo:9s} v={variant} tma={stg}x{tile:6d} ctas={ctas:4d} nsub={nsub:2d} "
+                        print(f"p={p} {coll:8s} {algo:9s} v={variant} tma={stg}x{tile:6d} thr={thr:3d} ctas={ctas:4d} nsub={nsub:2d} "
                               f"{us:9.1f} us {bw:7.1f} GB/s", flush=True)
-              world.set_param("ag_variant", 0)
-              world.set_param("rs_variant", 0)
+              world.set_param("ag_variant", -1)
+              world.set_param("rs_variant", -1)
     # NCCL reference points
     for coll in args.colls.split(","):
         kind, dt = coll.split("_")
