@@ -322,6 +322,68 @@ def run_gpu(args):
             ago = torch.empty(n_ag * p, dtype=torch.float32, device=dev)
             t = measure(lambda: dist.all_gather_into_tensor(ago, agi))
             extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
+            del nin, nout, agi, ago
+
+        # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
+        S_h = 256 << 20
+        grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
+        if grids:
+            n_h = S_h // 4 // p
+            if real:
+                h_ag_in, h_ag_out = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
+                h_rs_in, h_rs_out = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
+                h_ag_in.normal_()
+                h_rs_in.normal_()
+            else:
+                hai, hao = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
+                hri, hro = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
+                ptrs = {k: _lib.ptr_array([t.data_ptr() for t in v]) for k, v in
+                        dict(ai=hai, ao=hao, ri=hri, ro=hro).items()}
+            world.ensure_staging(int(L.pccl_staging_bytes(1, 3, p, n_h, 0)))
+            for (N, M) in grids:
+                inter = "recursive" if N >= 4 else "ring"
+                ia = _lib.ALGOS[inter]
+                if real:
+                    fa = lambda: _lib.check(L.pccl_hier_all_gather(world.handle, N, M, ia, h_ag_in.data_ptr(),  # noqa: E731
+                                                                  h_ag_out.data_ptr(), n_h, 0, stream.cuda_stream))
+                    fr = lambda: _lib.check(L.pccl_hier_reduce_scatter(world.handle, N, M, ia, h_rs_in.data_ptr(),  # noqa: E731
+                                                                      h_rs_out.data_ptr(), n_h, 0, stream.cuda_stream))
+                else:
+                    fa = lambda: _lib.check(L.pccl_emu_hier_all_gather(world.handle, N, M, ia, ptrs["ai"], ptrs["ao"],  # noqa: E731
+                                                                      n_h, 0, stream.cuda_stream))
+                    fr = lambda: _lib.check(L.pccl_emu_hier_reduce_scatter(world.handle, N, M, ia, ptrs["ri"],  # noqa: E731
+                                                                          ptrs["ro"], n_h, 0, stream.cuda_stream))
+                for nm, f in (("ag", fa), ("rs", fr)):
+                    t = measure(f)
+                    extra[f"hier_{nm}_f32_256MiB_{N}x{M}_{inter}"] = {"busbw_gbs": round(busbw(S_h, p, t), 1),
+                                                                      "us": round(t * 1e6, 1)}
+
+        # C5: FSDP / ZeRO-3 GPT-3-style 7B per-layer shapes (12h^2 + 13h params, h = 4096), bf16
+        if real:
+            P7 = 12 * 4096 * 4096 + 13 * 4096
+            n7 = P7 // p
+            S7 = n7 * p * 2
+            prm = world.empty(n7, torch.bfloat16)
+            full = world.empty(n7 * p, torch.bfloat16)
+            grad = world.empty(n7 * p, torch.bfloat16)
+            gsh = world.empty(n7, torch.bfloat16)
+            prm.normal_()
+            grad.normal_()
+            world.ensure_staging(int(L.pccl_staging_bytes(1, 2, p, n7, 1)))
+            t = measure(lambda: pkg.all_gather_into_tensor(full, prm, comm))
+            extra["fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
+                                             "bytes_out": S7, "algorithm": pkg.choose_algorithm("all_gather", p, S7)}
+            t = measure(lambda: pkg.reduce_scatter_tensor(gsh, grad, comm))
+            extra["fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
+                                             "bytes_in": S7, "algorithm": pkg.choose_algorithm("reduce_scatter", p, S7)}
+            nfull = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev)
+            nprm = torch.empty(n7, dtype=torch.bfloat16, device=dev).normal_()
+            t = measure(lambda: dist.all_gather_into_tensor(nfull, nprm))
+            extra["nccl_fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
+            ngrad = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev).normal_()
+            t = measure(lambda: dist.reduce_scatter_tensor(nprm, ngrad))
+            extra["nccl_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
+            del nfull, nprm, ngrad
 
     # ---- e2e through the public API with host buffers ----
     e2e = None if args.profile else run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)

@@ -340,3 +340,27 @@ def reduce_inplace(acc, other, op: ReduceOp = ReduceOp.SUM):
     else:
         np.copyto(acc, res.reshape(acc.shape))
     return acc
+
+
+# ---------------------------------------------------------------------------
+# torch.distributed-shaped wrappers for FSDP / ZeRO-3
+# ---------------------------------------------------------------------------
+def all_gather_into_tensor(output: torch.Tensor, input: torch.Tensor, comm, *, algorithm: str = "auto"):
+    """``output[g*n:(g+1)*n] = input of rank g`` (same contract as
+    ``torch.distributed.all_gather_into_tensor``). Zero-copy when both tensors
+    come from ``comm.world.empty`` (parameters kept in symmetric memory);
+    in-place when ``input`` is this rank's slice of ``output``."""
+    if output.numel() != input.numel() * comm.size:
+        raise LengthMismatch(f"output has {output.numel()} elements, expected {input.numel() * comm.size}")
+    all_gather(comm, input, algorithm=algorithm, out=output)
+    return output
+
+
+def reduce_scatter_tensor(output: torch.Tensor, input: torch.Tensor, comm, *, algorithm: str = "auto",
+                          order: str = "ring"):
+    """``output = chunk(rank) of the sum of every rank's input`` (same contract
+    as ``torch.distributed.reduce_scatter_tensor`` with SUM)."""
+    if input.numel() != output.numel() * comm.size:
+        raise LengthMismatch(f"input has {input.numel()} elements, expected {output.numel() * comm.size}")
+    reduce_scatter(comm, input, algorithm=algorithm, order=order, out=output)
+    return output

@@ -58,7 +58,7 @@ struct LaunchParams {
   int variant;      // data-movement variant (experiments / tuning)
   int tma_stages;   // TMA ring depth
   uint32_t tma_tile;  // TMA tile bytes
-  int pad1;
+  int local_fence;  // 1: pull-kernel signals fence at gpu scope (data is in the writer's own HBM)
   int64_t timeout_ns;
   int64_t blk;              // units per sub-block
   int64_t sub_stride;       // stride between sub-blocks (shared layout)
@@ -267,6 +267,28 @@ __device__ __forceinline__ void cta_signal_mask(Ctx &c, uint32_t mask, int unit)
     st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
   trace_ev(c, TR_SIGNAL, unit);
 }
+// Pull kernels publish data that lives in the writer's OWN memory: once a
+// gpu-scope fence has made it visible at the writer's L2 (the point of
+// coherence every NVLink reader goes through), a relaxed system-scope flag
+// store suffices. MEMBAR.GPU costs a local L2 round trip instead of the
+// system-wide drain of MEMBAR.SYS. Entry signals (data written before the
+// launch) and exit signals (my remote loads have returned) need no fence.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void cta_signal_local(Ctx &c, int m, int unit) {
+  if (!c.P->local_fence) { cta_signal(c, m, unit); return; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_gpu();
+    st_relaxed_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
+  }
+  trace_ev(c, TR_SIGNAL, unit);
+}
+__device__ __forceinline__ void cta_signal_entry(Ctx &c, uint32_t mask, int unit = 0) {
+  if (!c.P->local_fence) { cta_signal_mask(c, mask, unit); return; }
+  const int m = threadIdx.x;
+  if (m < c.gs && ((mask >> m) & 1u)) st_relaxed_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
+  trace_ev(c, TR_SIGNAL, unit);
+}
 // Kept for call-site symmetry: the signature now travels in the READY word.
 __device__ __forceinline__ void cta_publish_meta(const Ctx &, uint32_t) {}
 
@@ -276,7 +298,10 @@ __device__ __forceinline__ bool cta_exit(Ctx &c, uint32_t to, uint32_t from) {
   if (c.P->skip_exit) return true;
   __syncthreads();
   const int m = threadIdx.x;
-  if (m < c.gs && ((to >> m) & 1u)) st_release_sys(Ctx::word(c.slot_in(m), F_DONE, c.gi, c.b), c.epoch);
+  if (m < c.gs && ((to >> m) & 1u)) {
+    if (c.P->local_fence) st_relaxed_sys(Ctx::word(c.slot_in(m), F_DONE, c.gi, c.b), c.epoch);
+    else st_release_sys(Ctx::word(c.slot_in(m), F_DONE, c.gi, c.b), c.epoch);
+  }
   int code = 0;
   if (m < c.gs && ((from >> m) & 1u)) code = spin_ge(c, Ctx::word(c.my_slot, F_DONE, m, c.b), c.epoch);
   int ok = __syncthreads_and(code == 0);

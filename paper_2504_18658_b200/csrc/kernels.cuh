@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
   Ctx c = make_ctx(P);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   cta_publish_meta(c, peers);
-  cta_signal_mask(c, peers, 0);  // my send buffer is ready
+  cta_signal_entry(c, peers);  // my send buffer is ready
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ La
     int64_t lo, hi;
     cta_subslice(c, t, lo, hi);
     if (P.local_copy) ag_local_copy<U>(c, lo, hi);
-    cta_signal(c, next, t);
+    cta_signal_local(c, next, t);
   }
   char *my = P.recv[c.r];
   const char *pv = P.recv[c.world(prev)];
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ La
       for (int j = 0; j < P.nsubblk; ++j)
         copy_units<U, kUnroll>(ag_block<U>(P, my, c.y, blk, j), ag_block<U>(P, const_cast<char *>(pv), c.y, blk, j), lo,
                                hi);
-      if (s < gs - 1) cta_signal(c, next, s * nsub + t);
+      if (s < gs - 1) cta_signal_local(c, next, s * nsub + t);
     }
   }
   cta_exit(c, 1u << prev, 1u << next);
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
     int64_t lo, hi;
     cta_subslice(c, t, lo, hi);
     if (P.local_copy) ag_local_copy<U>(c, lo, hi);
-    cta_signal(c, recdbl_partner(c.gi, 0), t);
+    cta_signal_local(c, recdbl_partner(c.gi, 0), t);
   }
   char *my = P.recv[c.r];
   for (int k = 0; k < L; ++k) {
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
         for (int j = 0; j < P.nsubblk; ++j)
           copy_units<U, kUnroll>(ag_block<U>(P, my, c.y, i, j), ag_block<U>(P, const_cast<char *>(pr), c.y, i, j), lo,
                                  hi);
-      if (k + 1 < L) cta_signal(c, recdbl_partner(c.gi, k + 1), (k + 1) * nsub + t);
+      if (k + 1 < L) cta_signal_local(c, recdbl_partner(c.gi, k + 1), (k + 1) * nsub + t);
     }
   }
   cta_exit(c, partners, partners);
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   Ctx c = make_ctx(P);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   cta_publish_meta(c, peers);
-  cta_signal_mask(c, peers, 0);  // my recv may be written
+  cta_signal_entry(c, peers);  // my recv may be written
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (!cta_wait_mask(c, peers, 0, true)) return;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ La
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, 1u << next);
-  for (int t = 0; t < nsub; ++t) cta_signal(c, next, t);  // my send is ready
+  cta_signal_entry(c, 1u << next, nsub - 1);  // my send is ready (units 0..nsub-1)
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
   const int pw = c.world(prev);
   for (int s = 1; s < gs; ++s) {
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ La
         reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, sendp, c.y, ch, j),
                                         rs_chunk<T>(P, const_cast<char *>(remote), c.y, ch, j), lo, hi);
       }
-      if (!last) cta_signal(c, next, s * nsub + t);
+      if (!last) cta_signal_local(c, next, s * nsub + t);
     }
   }
   cta_exit(c, 1u << prev, 1u << next);
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
   cta_publish_meta(c, partners);
-  for (int t = 0; t < nsub; ++t) cta_signal(c, rechalf_partner(c.gi, gs, 0), t);  // my send is ready
+  cta_signal_entry(c, 1u << rechalf_partner(c.gi, gs, 0), nsub - 1);  // my send is ready (units 0..nsub-1)
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
   int lo_c = 0, hi_c = gs;
   for (int k = 0; k < L; ++k) {
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
           reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, const_cast<char *>(local), c.y, ch, j),
                                           rs_chunk<T>(P, const_cast<char *>(remote), c.y, ch, j), lo, hi);
         }
-      if (!last) cta_signal(c, rechalf_partner(c.gi, gs, k + 1), (k + 1) * nsub + t);
+      if (!last) cta_signal_local(c, rechalf_partner(c.gi, gs, k + 1), (k + 1) * nsub + t);
     }
     lo_c = m0;
     hi_c = m1;
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, (1u << next) | (1u << prev));
-  cta_signal(c, prev, 0);  // my recv is free
+  cta_signal_entry(c, 1u << prev);  // my recv is free
   if (!cta_wait(c, next, 0, true)) return;
   char *my = P.recv[c.r];
   char *nx = P.recv[c.world(next)];
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
   cta_publish_meta(c, partners);
-  cta_signal_mask(c, partners, 0);  // my recv is free
+  cta_signal_entry(c, partners);  // my recv is free
   char *my = P.recv[c.r];
   for (int k = 0; k < L; ++k) {
     const int partner = recdbl_partner(c.gi, k);
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring_push(const __grid_constant
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, (1u << next) | (1u << prev));
-  cta_signal(c, prev, 0);  // my staging is free
+  cta_signal_entry(c, 1u << prev);  // my staging is free
   if (!cta_wait(c, next, 0, true)) return;
   char *sendp = P.send[c.r], *stg = P.recv[c.r], *nstg = P.recv[c.world(next)], *outp = P.out[c.r];
   {
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant_
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
   cta_publish_meta(c, partners);
-  cta_signal_mask(c, partners, 0);  // my staging is free
+  cta_signal_entry(c, partners);  // my staging is free
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r], *stgp = P.recv[c.r];
   // staging slot of absolute chunk ch received at step k (region base = gs - gs/2^k chunks)
   auto stg_chunk = [&](char *buf, int k, int lo_k, int ch, int j) -> char * {
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   const int gs = c.gs, gi = c.gi;
   const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
   cta_publish_meta(c, peers);
-  cta_signal_mask(c, peers, 0);  // pull: my send is ready; push: my staging is free
+  cta_signal_entry(c, peers);  // pull: my send is ready; push: my staging is free
   if (!cta_wait_mask(c, peers, 0, true)) return;
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);

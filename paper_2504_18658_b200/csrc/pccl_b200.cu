@@ -50,6 +50,7 @@ struct pccl_world {
   int64_t p_tma_tile = 65536;
   int64_t p_timeout_ms = 20000;
   int64_t p_trace = 0;
+  int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
   uint32_t meta_skew[PCCL_MAXR] = {};
@@ -230,6 +231,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.err = w->err_dev;
   P.nsub = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_nsub, 32));
   P.variant = pl.variant;
+  P.local_fence = (int)w->p_local_fence;
   P.tma_stages = (int)w->p_tma_stages;
   P.tma_tile = (uint32_t)w->p_tma_tile;
 
@@ -799,6 +801,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_CTAS")) w->p_ctas = atoi(t);
   if (const char *t = getenv("PCCL_NSUB")) w->p_nsub = atoi(t);
   if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
+  if (const char *t = getenv("PCCL_LOCAL_FENCE")) w->p_local_fence = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
   if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
   if (const char *t = getenv("PCCL_TMA_STAGES")) w->p_tma_stages = atoi(t);
@@ -884,6 +887,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "tma_tile")) return &w->p_tma_tile;
   if (!strcmp(key, "timeout_ms")) return &w->p_timeout_ms;
   if (!strcmp(key, "trace")) return &w->p_trace;
+  if (!strcmp(key, "local_fence")) return &w->p_local_fence;
   return nullptr;
 }
 
