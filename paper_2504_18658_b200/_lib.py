@@ -10,7 +10,7 @@ import threading
 
 from .errors import STATUS_TO_ERROR, CollkitError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libpccl_b200.so")
+LIB_PATH = os.environ.get("PCCL_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libpccl_b200.so")
 IPC_HANDLE_BYTES = 64
 MAX_RANKS = 16
 

@@ -22,7 +22,10 @@
 namespace pccl {
 
 constexpr int kThreads = 512;
-constexpr int kUnroll = 4;
+#ifndef PCCL_UNROLL
+#define PCCL_UNROLL 8
+#endif
+constexpr int kUnroll = PCCL_UNROLL;
 
 __device__ __forceinline__ int ilog2(int x) { return 31 - __clz(x); }
 

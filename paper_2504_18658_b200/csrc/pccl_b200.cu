@@ -336,10 +336,11 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   const int threads = (int)std::max<int64_t>(64, std::min<int64_t>(w->p_threads, kThreads));
   int ctas = (int)w->p_ctas;
   if (ctas <= 0) {
-    // auto (measured, tools/sweep.py at p=4): latency-bound small messages
-    // want few CTAs (fewer flags), >= 32 MiB wants ~one CTA per SM.
+    // auto (measured, tools/sweep.py at p=2/4, profiles/r1_sweep_p*.csv):
+    // latency-bound small messages want fewer CTAs (fewer flags); >= 16 MiB
+    // wants ~one CTA per SM.
     const double S = (double)pl.gs * (double)pl.count * (double)es;
-    ctas = w->emu ? PCCL_MAX_CTAS : (S >= 32.0 * (1 << 20) ? 128 : S >= 4.0 * (1 << 20) ? 64 : S >= 2.0 * (1 << 20) ? 32 : 16);
+    ctas = w->emu ? PCCL_MAX_CTAS : (S >= 16.0 * (1 << 20) ? 128 : S >= 4.0 * (1 << 20) ? 64 : 48);
   }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
   {
