@@ -393,8 +393,7 @@ struct Binder {
     *off_out = off;
     return w->segs[w->staging].ptr[r] + off;
   }
-  void fill(int r, int seg, size_t off, char *const *dst_unused, char **per, char *own) {
-    (void)dst_unused;
+  void fill(int r, int seg, size_t off, char **per, char *own) {
     for (int q = 0; q < w->nranks; ++q) {
       if (w->emu && q != r) continue;  // emulation: each row binds its own rank only
       per[q] = w->segs[seg].ptr[q] ? w->segs[seg].ptr[q] + off : nullptr;
@@ -411,14 +410,14 @@ struct Binder {
       return true;
     }
     if (resolve(w, r, user, bytes, &seg, &off)) {
-      fill(r, seg, off, nullptr, per, (char *)user);
+      fill(r, seg, off, per, (char *)user);
       place = place * 31u + (uint32_t)seg * 7919u + (uint32_t)(off >> 8) + 1u;
       return true;
     }
     size_t soff;
     char *p = stage(r, bytes, &soff);
     if (!p) return false;
-    fill(r, w->staging, soff, nullptr, per, p);
+    fill(r, w->staging, soff, per, p);
     place = place * 31u + 17u;
     if (copy_in && cudaMemcpyAsync(p, user, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) {
       status = PCCL_ERR_CUDA;
@@ -432,7 +431,7 @@ struct Binder {
     size_t soff;
     char *p = stage(r, bytes, &soff);
     if (!p) return false;
-    fill(r, w->staging, soff, nullptr, per, p);
+    fill(r, w->staging, soff, per, p);
     return true;
   }
 };
@@ -599,8 +598,7 @@ std::vector<int> one(int r) { return std::vector<int>{r}; }
 pccl_comm *cached_group(pccl_world *w, const std::vector<int> &members, int comm_id) {
   uint32_t mask = 0;
   for (int m : members) mask |= 1u << m;
-  // key also on order: same set, different order would need its own object
-  uint32_t key = mask;
+  const uint32_t key = mask;  // one cached object per member set (order checked below)
   auto it = w->comm_cache.find(key);
   if (it != w->comm_cache.end()) {
     bool same = it->second->gs == (int)members.size();
