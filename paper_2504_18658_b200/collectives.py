@@ -112,8 +112,10 @@ def _finish(arg: _In, host: torch.Tensor):
 
 
 def _check_world_size_growth(comm, need: int, what: str):
+    """Segments grow collectively: only a world-sized call (every rank
+    present) may grow them in real mode; emulated worlds grow locally."""
     world = comm.world
-    if comm.size == world.nranks:
+    if comm.size == world.nranks or world.emulated:
         return True
     seg = world.staging if what == "staging" else world.io
     if seg is None or seg.nbytes < need:

@@ -92,6 +92,21 @@ def main() -> int:
             failures.append(f"reuse_{it}")
     comm.barrier()
 
+    # random launch skew between ranks: the device handshakes absorb it
+    import random
+    import time
+
+    rnd = random.Random(rank)
+    x = torch.full((8192 * p,), float(rank + 1), device="cuda")
+    for it in range(40):
+        torch.cuda.synchronize()
+        time.sleep(rnd.random() * 0.003)
+        algo = ["direct", "ring", "recursive" if pow2 else "direct"][it % 3]
+        y = pkg.reduce_scatter(comm, x, algorithm=algo)
+        z = pkg.all_gather(comm, y, algorithm=algo)
+        if float(y[0]) != p * (p + 1) / 2 or float(z[-1]) != p * (p + 1) / 2:
+            failures.append(f"skew_{it}")
+
     # cross-rank length mismatch must raise LengthMismatch (device-side check)
     from paper_2504_18658_b200.errors import LengthMismatch
 
