@@ -71,6 +71,10 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._thread = threading.Thread(target=self._read, daemon=True)
             self._thread.start()
+            t0 = time.time()  # nvidia-smi takes ~1-2 s to start: wait for its first sample
+            while not self.samples and time.time() - t0 < 8.0 and self._proc.poll() is None:
+                time.sleep(0.05)
+            self._skip = len(self.samples)  # samples before the load starts are not reported
         except OSError:
             self._proc = None
         return self
@@ -91,6 +95,7 @@ class Clocks:
             self._thread.join(timeout=2)
 
     def summary(self):
+        self.samples = self.samples[getattr(self, "_skip", 0):]
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
         sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
@@ -243,10 +248,19 @@ def run_gpu(args):
     # ---- soak (for the clock sampler), warmup, timed region ----
     clocks = Clocks(local_rank)
     with clocks:
-        t_end = time.time() + (0.0 if args.profile else 1.0)
-        while time.time() < t_end:
-            for _ in range(20):
+        # ~1 s of load for the clock sampler. The call count must be the same
+        # on every rank (SPMD: each rank issues the same collectives), so it is
+        # derived from a max-over-ranks estimate, never from local wall clock.
+        if not args.profile:
+            t_est = time_calls(call, 5, stream)
+            if real:
+                tt = torch.tensor([t_est], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_est = float(tt.item())
+            for i in range(max(20, min(20000, int(1.0 / max(t_est, 1e-6))))):
                 call()
+                if i % 50 == 49:
+                    torch.cuda.synchronize()
             torch.cuda.synchronize()
         for _ in range(args.warmup):
             call()

@@ -126,7 +126,15 @@ struct Ctx {
   }
 };
 
+// Programmatic dependent launch: let the next collective's grid be scheduled
+// while this one drains, and wait for the previous grid's completion (and
+// memory flush) before touching anything. No-ops without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
+  pdl_wait();
+  pdl_launch_dependents();
   Ctx c;
   c.P = &P;
   c.y = blockIdx.y;

@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j) {
-        const char *src = (s == 0) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U : ag_block<U>(P, my, c.y, blk, j);
+        // my own block comes from send, or is already in place in recv (local_copy == 0)
+        const char *src = (s == 0 && P.local_copy) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U
+                                                   : ag_block<U>(P, my, c.y, blk, j);
         copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), src, lo, hi);
       }
       cta_signal(c, next, push_unit(s, nsub, t));
@@ -376,7 +378,8 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
       cta_subslice(c, t, lo, hi);
       for (int i = start; i < start + width; ++i)
         for (int j = 0; j < P.nsubblk; ++j) {
-          const char *src = (i == c.gi) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U : ag_block<U>(P, my, c.y, i, j);
+          const char *src = (i == c.gi && P.local_copy) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U
+                                                        : ag_block<U>(P, my, c.y, i, j);
           copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), src, lo, hi);
         }
       cta_signal(c, partner, push_unit(k, nsub, t));

@@ -50,6 +50,7 @@ struct pccl_world {
   int64_t p_tma_tile = 65536;
   int64_t p_timeout_ms = 20000;
   int64_t p_trace = 0;
+  int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
@@ -364,6 +365,18 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   if (w->emu) {
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k, grid, block, args, smem, stream));
+  } else if (w->p_pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k, P));
   } else {
     k<<<grid, block, smem, stream>>>(P);
     CK(cudaGetLastError());
@@ -645,6 +658,7 @@ int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector
     pl.blk = (int64_t)count; pl.istride = (int64_t)M * count; pl.send_sub_stride = (int64_t)count;
     pl.local_copy = 1;
     pl.place = place;
+    pl.variant = w->p_ag_variant == 0 ? 0 : 1;  // push (recv is symmetric)
     for (size_t i = 0; i < ranks.size(); ++i) {
       const int r = ranks[i], j = r % M;
       std::vector<int> mem;
@@ -671,6 +685,7 @@ int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector
     pl.coll = PCCL_ALL_GATHER; pl.algo = A_RING; pl.dtype = dtype; pl.count = (size_t)N * count; pl.gs = M;
     pl.nsubblk = N; pl.blk = (int64_t)count; pl.sub_stride = (int64_t)M * count; pl.istride = (int64_t)count;
     pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
+    pl.variant = w->p_ag_variant == 0 ? 0 : 1;
     for (size_t i = 0; i < ranks.size(); ++i) {
       const int r = ranks[i], n = r / M;
       std::vector<int> mem;
@@ -722,7 +737,13 @@ int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::ve
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
     }
-    for (int q = 0; q < w->nranks; ++q) { pl.send[q] = sendp[q]; pl.work[q] = work[q]; pl.out[q] = part[q]; }
+    pl.variant = w->p_rs_variant == 1 ? 1 : 0;  // pull by default (measured faster here); push: staging = work
+    for (int q = 0; q < w->nranks; ++q) {
+      pl.send[q] = sendp[q];
+      pl.work[q] = work[q];
+      pl.recv[q] = work[q];
+      pl.out[q] = part[q];
+    }
     int s = launch(w, pl, stream);
     if (s) return s;
   } else {
@@ -745,7 +766,12 @@ int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::ve
       pl.rows.push_back({r, g});
       pl.out[r] = (char *)recvs[i];
     }
-    for (int q = 0; q < w->nranks; ++q) { pl.send[q] = part[q]; pl.work[q] = work2[q]; }
+    pl.variant = w->p_rs_variant == 1 ? 1 : 0;
+    for (int q = 0; q < w->nranks; ++q) {
+      pl.send[q] = part[q];
+      pl.work[q] = work2[q];
+      pl.recv[q] = work2[q];
+    }
     return launch(w, pl, stream);
   }
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -801,6 +827,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_NSUB")) w->p_nsub = atoi(t);
   if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
   if (const char *t = getenv("PCCL_LOCAL_FENCE")) w->p_local_fence = atoi(t);
+  if (const char *t = getenv("PCCL_PDL")) w->p_pdl = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
   if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
   if (const char *t = getenv("PCCL_TMA_STAGES")) w->p_tma_stages = atoi(t);
@@ -887,6 +914,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "timeout_ms")) return &w->p_timeout_ms;
   if (!strcmp(key, "trace")) return &w->p_trace;
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
+  if (!strcmp(key, "pdl")) return &w->p_pdl;
   return nullptr;
 }
 
