@@ -248,7 +248,7 @@ def run_gpu(args):
     # ---- soak (for the clock sampler), warmup, timed region ----
     clocks = Clocks(local_rank)
     with clocks:
-        # ~1 s of load for the clock sampler. The call count must be the same
+        # ~3 s of load for the clock sampler. The call count must be the same
         # on every rank (SPMD: each rank issues the same collectives), so it is
         # derived from a max-over-ranks estimate, never from local wall clock.
         if not args.profile:
@@ -257,7 +257,7 @@ def run_gpu(args):
                 tt = torch.tensor([t_est], device=dev, dtype=torch.float64)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t_est = float(tt.item())
-            for i in range(max(20, min(20000, int(1.0 / max(t_est, 1e-6))))):
+            for i in range(max(20, min(60000, int(3.0 / max(t_est, 1e-6))))):
                 call()
                 if i % 50 == 49:
                     torch.cuda.synchronize()
@@ -415,9 +415,15 @@ def run_gpu(args):
         hbm = rs_algorithmic_hbm_bytes(algo, p, n * es)
         achieved = hbm / t_call / 1e9
         peak = float(pk.get("hbm_gbs", 6650.0))
+        traffic = args.traffic
+        if traffic is None and algo == "recursive" and args.dtype == "bf16" and args.size_mib == 128:
+            # dram__bytes_read.sum + dram__bytes_write.sum of this launch, ncu --set full
+            # (profiles/r1_ncu_k_rs_rec_emulated.md): 1.878925 GB + 0.907570 GB
+            traffic = 2786495432
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                "algorithmic_bytes_per_launch": hbm, "traffic": args.traffic}
+                "algorithmic_bytes_per_launch": hbm, "traffic": traffic,
+                "traffic_source": "ncu --set full capture, profiles/r1_ncu_k_rs_rec_emulated.md" if traffic else None}
 
     cpu = None
     if rank == 0 and not real and not args.no_cpu:
