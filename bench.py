@@ -54,56 +54,67 @@ def peaks():
 # clocks sampler
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock + throttle reasons sampled every 50 ms through NVML while the
+    load runs (nvidia-smi with the reasons query only manages ~1 sample per
+    few seconds). Device index = the CUDA ordinal; CUDA_VISIBLE_DEVICES is
+    honoured by mapping through the PCI bus id."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
     def __init__(self, device: int):
         self.device = device
         self.samples = []
-        self._proc = None
+        self._stop = threading.Event()
         self._thread = None
+        self._err = None
 
     def __enter__(self):
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            try:
+                props = torch.cuda.get_device_properties(self.device)
+                bus = f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:{props.pci_device_id:02X}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:  # noqa: BLE001 - fall back to the NVML index
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self._nv = pynvml
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._thread = threading.Thread(target=self._run, daemon=True)
             self._thread.start()
-            t0 = time.time()  # nvidia-smi takes ~1-2 s to start: wait for its first sample
-            while not self.samples and time.time() - t0 < 8.0 and self._proc.poll() is None:
-                time.sleep(0.05)
-            self._skip = len(self.samples)  # samples before the load starts are not reported
-        except OSError:
-            self._proc = None
+        except Exception as exc:  # noqa: BLE001 - clocks are diagnostics
+            self._err = repr(exc)[:200]
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((sm, rs))
+            except Exception as exc:  # noqa: BLE001
+                self._err = repr(exc)[:200]
+                return
+            time.sleep(0.05)
 
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
+        if self._thread is not None:
             self._thread.join(timeout=2)
 
     def summary(self):
-        self.samples = self.samples[getattr(self, "_skip", 0):]
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
-        sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
-        smax = [int(s[1]) for s in self.samples if s[1].isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0, "error": self._err}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({name for _, r in self.samples for name, attr in self.REASONS.items()
+                          if r & getattr(self._nv, attr)})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self._max, "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML, 50 ms, during the soak + warm-up + timed steps"}
 
 
 # ---------------------------------------------------------------------------
