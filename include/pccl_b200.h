@@ -18,7 +18,12 @@
  * member issues the same collectives in the same order
  * (collkit/transport/base.py:131-134), which is what keeps the per-group epoch
  * counters (the replacement for next_base_tag) in agreement without any
- * host-side coordination.
+ * host-side coordination. Epochs live in device memory, so every collective
+ * is CUDA-graph capturable (segments must be sized before capture). All calls
+ * on one member set must be ordered on the device (one stream, or streams
+ * ordered with events): two concurrent collectives on the same group share its
+ * epoch word and corrupt each other, exactly like two unordered NCCL calls on
+ * one communicator.
  */
 #ifndef PCCL_B200_H
 #define PCCL_B200_H
@@ -92,7 +97,8 @@ int pccl_version(void);
 int pccl_world_create(int nranks, int rank, int device, pccl_world_t *out);
 int pccl_emu_world_create(int nranks, int device, pccl_world_t *out);
 int pccl_world_destroy(pccl_world_t w);
-int pccl_world_check(pccl_world_t w);           /* device-reported error, then cleared */
+int pccl_world_check(pccl_world_t w);           /* device-reported error (sticky until reset) */
+int pccl_world_error_detail(pccl_world_t w, int *out16); /* [8]=set,[9]=epoch,[10]=my hash,[11]=seen hash,[12]=rank,[13]=unit,[14]=seen unit,[15]=cta */
 int pccl_world_reset_flags(pccl_world_t w);      /* zero flags + epochs (emulation, after an error) */
 int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
@@ -128,6 +134,9 @@ int pccl_comm_create(pccl_world_t w, const int *members, int nmembers, int comm_
 int pccl_comm_destroy(pccl_comm_t c);
 int pccl_comm_size(pccl_comm_t c, int *size);
 int pccl_comm_rank(pccl_comm_t c, int *rank);
+/* Completed-call counter of the group, read from member `member`'s device
+ * memory (real mode: this rank only). Equal on every member between calls. */
+int pccl_comm_epoch(pccl_comm_t c, int member, uint64_t *epoch);
 
 /* ---- flat collectives (real mode: this rank's buffers) -----------------
  * pccl_all_gather replaces ring_all_gather / recdbl_all_gather

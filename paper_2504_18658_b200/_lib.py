@@ -33,6 +33,7 @@ _SIGS = {
     "pccl_emu_world_create": (_i, [_i, _i, ctypes.POINTER(_vp)]),
     "pccl_world_destroy": (_i, [_vp]),
     "pccl_world_check": (_i, [_vp]),
+    "pccl_world_error_detail": (_i, [_vp, ctypes.POINTER(_i)]),
     "pccl_world_reset_flags": (_i, [_vp]),
     "pccl_world_set_tuning": (_i, [_vp, _i, _i, _i]),
     "pccl_world_set_timeout_ms": (_i, [_vp, ctypes.c_int64]),
@@ -50,6 +51,7 @@ _SIGS = {
     "pccl_comm_destroy": (_i, [_vp]),
     "pccl_comm_size": (_i, [_vp, ctypes.POINTER(_i)]),
     "pccl_comm_rank": (_i, [_vp, ctypes.POINTER(_i)]),
+    "pccl_comm_epoch": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_uint64)]),
     "pccl_all_gather": (_i, [_vp, _i, _vp, _vp, _sz, _i, _vp]),
     "pccl_reduce_scatter": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _vp]),
     "pccl_hier_all_gather": (_i, [_vp, _i, _i, _i, _vp, _vp, _sz, _i, _vp]),

@@ -134,6 +134,13 @@ class Communicator:
     def device(self) -> torch.device:
         return torch.device("cuda", self.world.device)
 
+    def epoch(self) -> int:
+        """Completed collectives on this member set (device counter; equal on
+        every member between calls — the SPMD invariant)."""
+        e = ctypes.c_uint64()
+        check(lib().pccl_comm_epoch(self.handle, self.rank, ctypes.byref(e)), "comm_epoch")
+        return e.value
+
     def next_base_tag(self) -> int:
         """Same numbering as the reference (transport/base.py:131-138); the
         device epoch of the group advances in lockstep with it."""

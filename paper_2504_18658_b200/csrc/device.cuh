@@ -31,7 +31,8 @@
 #endif
 #define PCCL_MAX_CTAS 320
 #define PCCL_NSLOTS 256
-#define PCCL_SLOT_WORDS (3 * PCCL_MAXR * PCCL_MAX_CTAS)
+#define PCCL_CTRL_OFF (3 * PCCL_MAXR * PCCL_MAX_CTAS)
+#define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
 #define PCCL_FLAG_BYTES ((size_t)PCCL_NSLOTS * PCCL_SLOT_BYTES)
 #define PCCL_ABORT_BIT (1ull << 63)
@@ -142,14 +143,34 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.gi = P.grank[c.y];
   c.gs = P.gs;
   c.b = blockIdx.x;
-  c.epoch = P.epoch[c.y];
   c.my_slot = P.flags[c.r] + P.slot_off[c.y];
+  // The group's epoch lives in device memory (CTRL[0] of my slot): read it at
+  // launch, the last CTA to exit advances it. No host bookkeeping, so a
+  // captured CUDA graph replays correctly.
+  c.epoch = *reinterpret_cast<volatile uint64_t *>(c.my_slot + PCCL_CTRL_OFF) + 1;
   c.t0 = global_timer_ns();
   c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
   c.ntr = 0;
   if (c.tr && threadIdx.x == 0) c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
   return c;
 }
+
+// Runs when a kernel returns (any path): the last CTA of the row to leave
+// publishes the epoch for the next launch on this stream.
+struct CtaEpilogue {
+  const Ctx &c;
+  __device__ explicit CtaEpilogue(const Ctx &cc) : c(cc) {}
+  __device__ ~CtaEpilogue() {
+    if (threadIdx.x == 0) {
+      unsigned long long *ctrl = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF);
+      const unsigned long long old = atomicAdd(ctrl + 1, 1ull);
+      if (old == (unsigned long long)(c.P->ctas - 1)) {
+        ctrl[1] = 0;
+        *reinterpret_cast<volatile unsigned long long *>(ctrl) = c.epoch;
+      }
+    }
+  }
+};
 
 // thread 0 only: append (time, kind, unit) to this CTA's trace
 __device__ __forceinline__ void trace_ev(Ctx &c, int kind, int unit) {
@@ -208,7 +229,19 @@ __device__ __forceinline__ int ready_check(const Ctx &c, uint64_t v, int unit) {
   const uint64_t ep = (v >> 32) & 0x7fffffffull;
   if (ep > c.epoch) return 0;
   if (ep < c.epoch) return -1;
-  if (((v >> 10) & 0x3fffffu) != (c.P->meta[c.y] & 0x3fffffu)) return 4;  // PCCL_ERR_LENGTH_MISMATCH
+  if (((v >> 10) & 0x3fffffu) != (c.P->meta[c.y] & 0x3fffffu)) {
+    // diagnostics for pccl_world_error_detail: first mismatch only
+    if (atomicCAS((int *)&c.P->err[8], 0, 1) == 0) {
+      c.P->err[9] = (int)c.epoch;
+      c.P->err[10] = (int)(c.P->meta[c.y] & 0x3fffffu);
+      c.P->err[11] = (int)((v >> 10) & 0x3fffffu);
+      c.P->err[12] = c.r;
+      c.P->err[13] = unit;
+      c.P->err[14] = (int)(v & 0x3ffu);
+      c.P->err[15] = c.b;
+    }
+    return 4;  // PCCL_ERR_LENGTH_MISMATCH
+  }
   return (v & 0x3ffu) >= (uint64_t)(unit + 1) ? 0 : -1;
 }
 __device__ __forceinline__ int spin_ready(const Ctx &c, const uint64_t *w, int unit) {

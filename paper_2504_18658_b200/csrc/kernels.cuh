@@ -50,6 +50,7 @@ __device__ __forceinline__ void ag_local_copy(const Ctx &c, int64_t lo, int64_t 
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   cta_publish_meta(c, peers);
   cta_signal_entry(c, peers);  // my send buffer is ready
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, 1u << next);
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ La
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
@@ -155,6 +158,7 @@ __device__ __forceinline__ void store_units(char *dst, const char *src, int64_t 
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   cta_publish_meta(c, peers);
   cta_signal_entry(c, peers);  // my recv may be written
@@ -195,6 +199,7 @@ template <bool PUSH>
 __global__ void __launch_bounds__(kThreads) k_ag_direct_tma(const __grid_constant__ LaunchParams P) {
   extern __shared__ __align__(128) char dsm[];
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   TmaRing R = tma_ring_setup(dsm, P.tma_stages, P.tma_tile);
   cta_publish_meta(c, peers);
@@ -246,6 +251,7 @@ template <int DT, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ LaunchParams P) {
   using T = typename RUnit<DT, VEC>::T;
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, 1u << next);
@@ -275,6 +281,7 @@ template <int DT, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ LaunchParams P) {
   using T = typename RUnit<DT, VEC>::T;
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
@@ -326,6 +333,7 @@ __device__ __forceinline__ int push_unit(int step, int nsub, int t) { return 1 +
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, (1u << next) | (1u << prev));
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
 template <int U>
 __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant__ LaunchParams P) {
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
@@ -400,6 +409,7 @@ template <int DT, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_ring_push(const __grid_constant__ LaunchParams P) {
   using T = typename RUnit<DT, VEC>::T;
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
   cta_publish_meta(c, (1u << next) | (1u << prev));
@@ -440,6 +450,7 @@ template <int DT, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant__ LaunchParams P) {
   using T = typename RUnit<DT, VEC>::T;
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
@@ -532,6 +543,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   using T = typename R::T;
   using Acc = typename R::Acc;
   Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
   const int gs = c.gs, gi = c.gi;
   const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
   cta_publish_meta(c, peers);

@@ -50,6 +50,7 @@ struct pccl_world {
   int64_t p_tma_tile = 65536;
   int64_t p_timeout_ms = 20000;
   int64_t p_trace = 0;
+  int poisoned = 0;  // sticky device error
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
@@ -306,7 +307,6 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
 
   // ---- rows
   const int nrows = (int)pl.rows.size();
-  std::map<int, uint64_t> slot_epoch;  // bump each group's epoch once per launch
   for (int y = 0; y < nrows; ++y) {
     const Row &rw = pl.rows[y];
     const pccl_comm *g = rw.g;
@@ -319,9 +319,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     P.grank[y] = (int8_t)gi;
     P.base[y] = units(pl.base[rw.rank]);
     P.slot_off[y] = (uint32_t)((size_t)g->slot * PCCL_SLOT_WORDS);
-    auto it = slot_epoch.find(g->slot);
-    if (it == slot_epoch.end()) it = slot_epoch.emplace(g->slot, ++w->epoch[g->slot]).first;
-    P.epoch[y] = it->second;
+    P.epoch[y] = 0;  // device-side (CTRL word of the slot), see make_ctx
     P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order, pl.count, pl.dtype, pl.gs) ^ (pl.place * 2654435761u) ^
                  w->meta_skew[rw.rank]) & 0x7fffffffu;
   }
@@ -449,13 +447,13 @@ struct Binder {
   }
 };
 
+// A device-reported error poisons the world: kernels that aborted did not
+// finish their protocol, so every later call fails fast with the same code
+// until pccl_world_reset_flags (emulation) or the world is recreated.
 int check_world_err(pccl_world *w) {
-  int e = *w->err_host;
-  if (e) {
-    *w->err_host = 0;
-    return e;
-  }
-  return PCCL_SUCCESS;
+  const int e = *w->err_host;
+  if (e && !w->poisoned) w->poisoned = e;
+  return w->poisoned;
 }
 
 // --------------------------------------------------------------------------
@@ -872,6 +870,12 @@ int pccl_world_destroy(pccl_world_t w) {
   return PCCL_SUCCESS;
 }
 
+int pccl_world_error_detail(pccl_world_t w, int *out16) {
+  if (!w || !out16) return PCCL_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < 16; ++i) out16[i] = w->err_host[i];
+  return PCCL_SUCCESS;
+}
+
 int pccl_world_check(pccl_world_t w) {
   if (!w) return PCCL_ERR_INVALID_ARGUMENT;
   return check_world_err(w);
@@ -885,7 +889,8 @@ int pccl_world_reset_flags(pccl_world_t w) {
     if (w->segs[0].ptr[q] && w->segs[0].owned[q]) CK(cudaMemset(w->segs[0].ptr[q], 0, PCCL_FLAG_BYTES));
   CK(cudaDeviceSynchronize());
   memset(w->epoch, 0, sizeof(w->epoch));
-  *w->err_host = 0;
+  for (int i = 0; i < 16; ++i) w->err_host[i] = 0;
+  w->poisoned = 0;
   return PCCL_SUCCESS;
 }
 
@@ -1076,6 +1081,18 @@ int pccl_comm_create(pccl_world_t w, const int *members, int n, int comm_id, pcc
     return PCCL_ERR_OUT_OF_MEMORY;
   }
   *out = c;
+  return PCCL_SUCCESS;
+}
+
+int pccl_comm_epoch(pccl_comm_t c, int member, uint64_t *epoch) {
+  if (!c || !epoch || member < 0 || member >= c->gs) return PCCL_ERR_INVALID_ARGUMENT;
+  pccl_world *w = c->w;
+  const int r = c->members[member];
+  if (!w->emu && r != w->rank) return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  CK(cudaDeviceSynchronize());
+  const uint64_t *ctrl = (const uint64_t *)w->segs[0].ptr[r] + (size_t)c->slot * PCCL_SLOT_WORDS + PCCL_CTRL_OFF;
+  CK(cudaMemcpy(epoch, ctrl, 8, cudaMemcpyDeviceToHost));
   return PCCL_SUCCESS;
 }
 

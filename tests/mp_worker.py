@@ -28,6 +28,21 @@ def main() -> int:
     p = world
     failures = []
 
+    def sync_point(name):
+        # device errors are sticky and async: surface them per section, and
+        # verify every rank completed the same number of collectives
+        torch.cuda.synchronize()
+        try:
+            comm.world.check()
+        except Exception as exc:  # noqa: BLE001
+            failures.append(f"{name}:{type(exc).__name__}")
+            raise
+        eps = [None] * p
+        dist.all_gather_object(eps, comm.epoch())
+        if len(set(eps)) != 1:
+            failures.append(f"{name}:epochs{eps}")
+            raise RuntimeError(f"epoch divergence after {name}: {eps}")
+
     def check(name, got, want):
         g = np.ascontiguousarray(got)
         w = np.ascontiguousarray(want)
@@ -53,6 +68,7 @@ def main() -> int:
             check(f"rs_rechalf_n{n}", pkg.rechalf_reduce_scatter(comm, rs_in[rank]), want)
             check(f"rs_direct_rec_n{n}", pkg.direct_reduce_scatter(comm, rs_in[rank], order="recursive"), want)
 
+    sync_point("flat")
     # bf16 on device tensors, both through staging and through symmetric buffers
     n = 65536 + 8
     ins = [oracle.f32_to_bf16(rng.standard_normal(n * p).astype(np.float32)) for _ in range(p)]
@@ -70,6 +86,7 @@ def main() -> int:
     got = pkg.reduce_scatter(comm, sym_in, algorithm="direct", out=sym_out)
     check("bf16_direct_symmetric", got.view(torch.int16).cpu().numpy().view(np.uint16), want)
 
+    sync_point("bf16")
     # hierarchical virtual nodes
     grids = [(N, p // N) for N in (1, 2, 4, 8) if p % N == 0]
     for N, M in grids:
@@ -84,6 +101,7 @@ def main() -> int:
             check(f"hier_rs_{N}x{M}_{inter}", pkg.hier_reduce_scatter(plan, comm, rs_in[rank]),
                   oracle.hier_reduce_scatter(rs_in, N, M, inter)[rank])
 
+    sync_point("hier")
     # back-to-back reuse + barrier
     for it in range(30):
         x = torch.full((4096 * p,), float(it + rank), device="cuda")
@@ -92,6 +110,7 @@ def main() -> int:
             failures.append(f"reuse_{it}")
     comm.barrier()
 
+    sync_point("reuse")
     # random launch skew between ranks: the device handshakes absorb it
     import random
     import time
@@ -106,6 +125,39 @@ def main() -> int:
         z = pkg.all_gather(comm, y, algorithm=algo)
         if float(y[0]) != p * (p + 1) / 2 or float(z[-1]) != p * (p + 1) / 2:
             failures.append(f"skew_{it}")
+
+    sync_point("skew")
+    # CUDA graph: capture collectives, replay, interleave with eager calls
+    from paper_2504_18658_b200 import _lib
+
+    L = _lib.lib()
+    gin = comm.world.empty(4096 * p, torch.float32)
+    gout = comm.world.empty(4096, torch.float32)
+    gag = comm.world.empty(4096 * p, torch.float32)
+    gin.copy_(torch.arange(4096 * p, dtype=torch.float32, device="cuda") * (rank + 1))
+    side = torch.cuda.Stream()
+    ga = _lib.ALGOS["recursive" if pow2 else "ring"]
+
+    def gstep(s):
+        _lib.check(L.pccl_reduce_scatter(comm.handle, ga, 0, gin.data_ptr(), gout.data_ptr(), 4096, 0, s))
+        _lib.check(L.pccl_all_gather(comm.handle, _lib.ALGOS["direct"], gout.data_ptr(), gag.data_ptr(), 4096, 0, s))
+
+    torch.cuda.synchronize()
+    gstep(side.cuda_stream)
+    side.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        gstep(side.cuda_stream)
+        gstep(side.cuda_stream)
+    with torch.cuda.stream(side):  # replay() launches on the current stream
+        for _ in range(20):
+            graph.replay()
+    gstep(side.cuda_stream)
+    sync_point("graph")
+    tot = p * (p + 1) / 2
+    want = torch.arange(4096 * p, dtype=torch.float32, device="cuda") * tot
+    if not torch.equal(gout, want[rank * 4096:(rank + 1) * 4096]) or not torch.equal(gag, want):
+        failures.append("cuda_graph")
 
     # cross-rank length mismatch must raise LengthMismatch (device-side check)
     from paper_2504_18658_b200.errors import LengthMismatch

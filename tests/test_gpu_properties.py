@@ -156,3 +156,52 @@ def test_subgroup_collectives_and_barrier():
         members = [m for m in range(p) if m % 2 == r % 2]
         assert np.array_equal(g, np.repeat(np.array(members, np.float32), 6))
         assert np.all(s == sum(members))
+
+
+@pytest.mark.parametrize("algo", ["direct", "ring", "recursive"])
+def test_cuda_graph_capture_and_replay(algo):
+    """Epochs live in device memory, so collectives captured into a CUDA graph
+    replay correctly, and eager calls interleave with replays."""
+    pkg = _pkg()
+    from paper_2504_18658_b200 import _lib
+    from paper_2504_18658_b200.communicator import _emu_group
+
+    p, n = 4, 1 << 16
+    w = pkg.emulated_world(p)
+    group, _ = _emu_group(w, tuple(range(p)), 0)
+    L = _lib.lib()
+    a = _lib.ALGOS[algo]
+    ins = w.empty(n * p, torch.float32)
+    outs = w.empty(n, torch.float32)
+    ag_out = w.empty(n * p, torch.float32)
+    for r in range(p):
+        ins[r].copy_(torch.arange(n * p, dtype=torch.float32) * (r + 1))
+    w.ensure_staging(int(L.pccl_staging_bytes(1, a, p, n, 0)) + int(L.pccl_staging_bytes(0, a, p, n, 0)))
+    sp = _lib.ptr_array([t.data_ptr() for t in ins])
+    rp = _lib.ptr_array([t.data_ptr() for t in outs])
+    ap = _lib.ptr_array([t.data_ptr() for t in ag_out])
+    stream = torch.cuda.Stream()
+    order = _lib.ORDERS["recursive" if algo == "recursive" else "ring"]
+
+    def step(s):
+        _lib.check(L.pccl_emu_reduce_scatter(group.handle, a, order, sp, rp, n, 0, s))
+        _lib.check(L.pccl_emu_all_gather(group.handle, a, rp, ap, n, 0, s))
+
+    torch.cuda.synchronize()
+    step(stream.cuda_stream)  # eager warm-up (also grows nothing during capture)
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        step(stream.cuda_stream)
+        step(stream.cuda_stream)
+    with torch.cuda.stream(stream):  # replay() launches on the current stream: keep one stream
+        for _ in range(25):
+            g.replay()
+    step(stream.cuda_stream)  # eager after replays
+    torch.cuda.synchronize()
+    w.check()
+    total = sum(range(1, p + 1))
+    want_rs = [torch.arange(n * p, dtype=torch.float32)[r * n:(r + 1) * n] * total for r in range(p)]
+    for r in range(p):
+        assert torch.equal(outs[r].cpu(), want_rs[r])
+        assert torch.equal(ag_out[r].cpu(), torch.cat(want_rs))
