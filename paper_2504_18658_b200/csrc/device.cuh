@@ -392,21 +392,24 @@ template <> struct VecT<1> { using T = unsigned char; };
 // during this kernel by another GPU and published through the flag protocol.
 template <typename T> __device__ __forceinline__ T ld_peer(const T *p) { return __ldcg(p); }
 
+// Every iteration keeps UNROLL independent loads in flight per thread, also
+// for the last partial iteration (predicated), so short slices do not fall
+// back to one outstanding load per thread.
 template <int U, int UNROLL>
 __device__ __forceinline__ void copy_units(char *dst, const char *src, int64_t lo, int64_t hi) {
   using T = typename VecT<U>::T;
   T *d = reinterpret_cast<T *>(dst);
   const T *s = reinterpret_cast<const T *>(src);
   const int nt = blockDim.x;
-  int64_t i = lo + threadIdx.x;
-  for (; i + (int64_t)(UNROLL - 1) * nt < hi; i += (int64_t)UNROLL * nt) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)UNROLL * nt) {
     T v[UNROLL];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) v[u] = ld_peer(s + i + (int64_t)u * nt);
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) v[u] = ld_peer(s + i + (int64_t)u * nt);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) d[i + (int64_t)u * nt] = v[u];
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) d[i + (int64_t)u * nt] = v[u];
   }
-  for (; i < hi; i += nt) d[i] = ld_peer(s + i);
 }
 
 // --------------------------------------------------------------------------
@@ -527,24 +530,22 @@ __device__ __forceinline__ void reduce2_units(char *dst, const char *a, const ch
   const T *x = reinterpret_cast<const T *>(a);
   const T *y = reinterpret_cast<const T *>(b);
   const int nt = blockDim.x;
-  int64_t i = lo + threadIdx.x;
-  for (; i + (int64_t)(UNROLL - 1) * nt < hi; i += (int64_t)UNROLL * nt) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)UNROLL * nt) {
     T vy[UNROLL], vx[UNROLL];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) vy[u] = ld_peer(y + i + (int64_t)u * nt);
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) vy[u] = ld_peer(y + i + (int64_t)u * nt);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) vx[u] = __ldcg(x + i + (int64_t)u * nt);
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) vx[u] = __ldcg(x + i + (int64_t)u * nt);
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      typename R::Acc s = R::load(vx[u]);
-      acc_add<typename R::Acc, R::N>(s, R::load(vy[u]));
-      d[i + (int64_t)u * nt] = R::store(s);
+      if (i + (int64_t)u * nt < hi) {
+        typename R::Acc sum = R::load(vx[u]);
+        acc_add<typename R::Acc, R::N>(sum, R::load(vy[u]));
+        d[i + (int64_t)u * nt] = R::store(sum);
+      }
     }
-  }
-  for (; i < hi; i += nt) {
-    typename R::Acc s = R::load(__ldcg(x + i));
-    acc_add<typename R::Acc, R::N>(s, R::load(ld_peer(y + i)));
-    d[i] = R::store(s);
   }
 }
 
