@@ -27,3 +27,25 @@ def test_real_mode_parity(nproc):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("OK") >= nproc, out[-4000:]
+
+
+@pytest.mark.parametrize("backend,algo,grid", [("b200", "ring", ""), ("b200", "hierarchical", "2x1"),
+                                               ("nccl", "auto", "")])
+def test_sweep_harness_real_mode(backend, algo, grid, tmp_path):
+    """The reference-style harness under torchrun: verified cells, one CSV."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    csv = tmp_path / "recs.csv"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29511", "-m", "paper_2504_18658_b200.sweep",
+           "--backend", backend, "--collective", "rs", "--algorithm", algo, "--sizes", "1MiB,4MiB",
+           "--trials", "3", "--warmup", "--verify", "--csv", str(csv)] + (["--grid", grid] if grid else [])
+    r = subprocess.run(cmd, env=dict(os.environ, PCCL_TIMEOUT_MS="10000"), capture_output=True, text=True,
+                       timeout=300, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    from paper_2504_18658_b200 import sweep as S
+
+    recs = S.read_records_csv(csv)
+    assert len(recs) == 2 * 4 and all(rec.verified and rec.backend == backend for rec in recs)
+    assert out.count("verified") == 2, out[-2000:]

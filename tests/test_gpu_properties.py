@@ -205,3 +205,52 @@ def test_cuda_graph_capture_and_replay(algo):
     for r in range(p):
         assert torch.equal(outs[r].cpu(), want_rs[r])
         assert torch.equal(ag_out[r].cpu(), torch.cat(want_rs))
+
+
+@pytest.mark.parametrize("p", [4, 8])
+@pytest.mark.parametrize("coll,algo", [("rs", "ring"), ("rs", "recursive"), ("rs", "direct"),
+                                       ("ag", "ring"), ("ag", "recursive"), ("ag", "direct")])
+def test_device_step_structure_matches_schedule(p, coll, algo):
+    """The kernels' own event trace (per CTA: waits on a peer, signals to a
+    peer) has exactly the step count of the algorithm's schedule
+    (pccl_schedule == collkit.simnet.build_schedule, tests/test_abi.py):
+    ring p-1 steps, recursive log2 p, direct 1."""
+    pkg = _pkg()
+    from paper_2504_18658_b200 import _lib
+    from paper_2504_18658_b200.communicator import _emu_group
+
+    w = pkg.emulated_world(p)
+    group, _ = _emu_group(w, tuple(range(p)), 0)
+    L = _lib.lib()
+    n = 1 << 14
+    a = _lib.ALGOS[algo]
+    ins = w.empty(n * p if coll == "rs" else n, torch.float32)
+    outs = w.empty(n if coll == "rs" else n * p, torch.float32)
+    w.ensure_staging(int(L.pccl_staging_bytes(1 if coll == "rs" else 0, a, p, n, 0)))
+    sp = _lib.ptr_array([t.data_ptr() for t in ins])
+    rp = _lib.ptr_array([t.data_ptr() for t in outs])
+    steps = len(_lib.schedule(1 if coll == "rs" else 0, a, 1, 1, p, n * p * 4))
+    try:
+        w.set_param("trace", 1)
+        w.set_param("nsub", 1)
+        s = torch.cuda.current_stream().cuda_stream
+        if coll == "rs":
+            _lib.check(L.pccl_emu_reduce_scatter(group.handle, a, 0, sp, rp, n, 0, s))
+        else:
+            _lib.check(L.pccl_emu_all_gather(group.handle, a, sp, rp, n, 0, s))
+        torch.cuda.synchronize()
+        tr = w.trace()
+    finally:
+        w.set_param("trace", 0)
+    assert len(tr) == p
+    # default data movement for symmetric buffers: AG push; RS ring push,
+    # recursive / direct pull. Waits per CTA = the algorithm's steps plus the
+    # push handshakes ("your buffer is free" before the first store, and the
+    # final arrival of the last forwarded block for AG).
+    L = steps
+    expect = {("rs", "ring"): L + 1, ("rs", "recursive"): L, ("rs", "direct"): L,
+              ("ag", "ring"): L + 1, ("ag", "recursive"): 2 * L, ("ag", "direct"): L + 1}[(coll, algo)]
+    for row in tr:
+        for ev in row:
+            kinds = [k for _, k, _ in ev]
+            assert kinds[0] == 1 and kinds.count(2) == expect, (coll, algo, p, kinds)
