@@ -551,6 +551,34 @@ __device__ __forceinline__ void reduce2_units(char *dst, const char *a, const ch
 
 
 // --------------------------------------------------------------------------
+// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
+// --------------------------------------------------------------------------
+struct alignas(32) V256 {
+  uint32_t x[8];
+};
+__device__ __forceinline__ V256 ld256_cg(const V256 *p) {
+  V256 v;
+  asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.x[0]), "=r"(v.x[1]), "=r"(v.x[2]), "=r"(v.x[3]), "=r"(v.x[4]), "=r"(v.x[5]), "=r"(v.x[6]),
+                 "=r"(v.x[7])
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ V256 ld256_nc(const V256 *p) {
+  V256 v;
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.x[0]), "=r"(v.x[1]), "=r"(v.x[2]), "=r"(v.x[3]), "=r"(v.x[4]), "=r"(v.x[5]), "=r"(v.x[6]),
+                 "=r"(v.x[7])
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st256(V256 *p, const V256 &v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.x[0]), "r"(v.x[1]), "r"(v.x[2]),
+               "r"(v.x[3]), "r"(v.x[4]), "r"(v.x[5]), "r"(v.x[6]), "r"(v.x[7])
+               : "memory");
+}
+
+// --------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk) + mbarriers: one elected thread moves large
 // tiles between global memory (local or NVLink-mapped peer) and shared memory
 // with almost no instruction overhead, so a few SMs keep MBs in flight.

@@ -633,7 +633,25 @@ __global__ void __launch_bounds__(kThreads) k_probe(char *local, const LaunchPar
   uint4 *rem = reinterpret_cast<uint4 *>(P.recv[q]);
   uint4 *loc = reinterpret_cast<uint4 *>(local);
   const int nt = blockDim.x;
-  if (mode == 0) {
+  if (mode >= 2) {  // 256-bit accesses (LDG/STG .256 on sm_100)
+    V256 *rem8 = reinterpret_cast<V256 *>(P.recv[q]);
+    V256 *loc8 = reinterpret_cast<V256 *>(local);
+    lo >>= 1; hi >>= 1;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
+      V256 v[kUnroll];
+      if (mode == 2) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) v[u] = ld256_nc(loc8 + i + u * nt);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) st256(rem8 + i + u * nt, v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) v[u] = ld256_cg(rem8 + i + u * nt);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) st256(loc8 + i + u * nt, v[u]);
+      }
+    }
+  } else if (mode == 0) {
     for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
       uint4 v[kUnroll];
 #pragma unroll

@@ -159,6 +159,17 @@ def main() -> int:
     if not torch.equal(gout, want[rank * 4096:(rank + 1) * 4096]) or not torch.equal(gag, want):
         failures.append("cuda_graph")
 
+    # online calibration: every rank must resolve "auto" identically afterwards
+    from paper_2504_18658_b200 import selector, tuning
+
+    tuned = tuning.autotune(comm, "reduce_scatter", 4 << 20, iters=3, warmup=1)
+    pick = selector.choose_algorithm("reduce_scatter", p, 4 << 20)
+    picks = [None] * p
+    dist.all_gather_object(picks, (pick, sorted(tuned)))
+    if len(set(map(str, picks))) != 1 or pick not in tuned or not all(v > 0 for v in tuned.values()):
+        failures.append(f"autotune {picks} {tuned}")
+    sync_point("autotune")
+
     # cross-rank length mismatch must raise LengthMismatch (device-side check)
     from paper_2504_18658_b200.errors import LengthMismatch
 

@@ -9,6 +9,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, torch.distributed as dist
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--pats", default="uni,bi,a2a,ring,one2all")
+    ap.add_argument("--modes", default="0,1", help="0 push16 1 pull16 2 push32 3 pull32 (bytes per access)")
+    ap.add_argument("--ctas", default="8,16,32,64,128")
+    a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"])); torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
@@ -22,12 +28,14 @@ def main():
     pats = {"uni": lambda r: (1 << 1) if r == 0 else 0, "bi": lambda r: (1 << (1 - r)) if r < 2 else 0,
             "a2a": lambda r: ((1 << p) - 1) & ~(1 << r), "ring": lambda r: 1 << ((r + 1) % p),
             "one2all": lambda r: (((1 << p) - 1) & ~1) if r == 0 else 0}
-    for pat, fm in pats.items():
-        for mode in (0, 1):
-            for ctas in (8, 16, 32, 64, 128):
+    names = {0: "push16", 1: "pull16", 2: "push32", 3: "pull32"}
+    for pat in a.pats.split(","):
+        fm = pats[pat]
+        for mode in map(int, a.modes.split(",")):
+            for ctas in map(int, a.ctas.split(",")):
                 mask = fm(rank)
                 npeers = bin(mask).count("1")
-                per = (B // max(1, npeers)) // 16 * 16
+                per = (B // max(1, npeers)) // 32 * 32
                 def f():
                     if mask:
                         _lib.check(L.pccl_probe(w.handle, seg.id, mode, mask, per, ctas, st.cuda_stream))
@@ -44,7 +52,7 @@ def main():
                 dist.all_gather(g, tt)
                 if rank == 0:
                     vals = [round(float(x), 1) for x in g]
-                    print(f"p={p} {pat:8s} {'push' if mode == 0 else 'pull'} ctas={ctas:4d} per-rank GB/s {vals}", flush=True)
+                    print(f"p={p} {pat:8s} {names[mode]} ctas={ctas:4d} per-rank GB/s {vals}", flush=True)
     dist.barrier(); dist.destroy_process_group()
 
 if __name__ == "__main__":
