@@ -254,3 +254,47 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
         for ev in row:
             kinds = [k for _, k, _ in ev]
             assert kinds[0] == 1 and kinds.count(2) == expect, (coll, algo, p, kinds)
+
+
+# ---------------------------------------------------------------------------
+# maximum sizes: byte offsets and element indices beyond 2^32 / 2^31
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("algo", ["direct", "ring", "recursive"])
+def test_offsets_beyond_4gib(algo):
+    """AG of 4 GiB + 4112 B per rank (output offsets past 2^33) and RS of
+    2^31 + 2^16 + 8 bf16 elements per rank (element indices past 2^31)."""
+    pkg = _pkg()
+    p = 2
+    torch.cuda.empty_cache()
+    n = (1 << 32) + 4112
+    g = torch.Generator(device="cuda").manual_seed(11)
+    ins = [torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda", generator=g) for _ in range(p)]
+    ag = {"direct": pkg.direct_all_gather, "ring": pkg.ring_all_gather, "recursive": pkg.recdbl_all_gather}[algo]
+    outs = [torch.empty(n * p, dtype=torch.uint8, device="cuda") for _ in range(p)]
+    pkg.run_ranks(p, lambda c: ag(c, ins[c.rank], out=outs[c.rank]))
+    for r in range(p):
+        for q in range(p):
+            assert torch.equal(outs[r][q * n:(q + 1) * n], ins[q]), (algo, r, q)
+    del ins, outs
+    torch.cuda.empty_cache()
+
+    m = (1 << 31) + (1 << 16) + 8  # RS input elements per rank (bf16)
+    ins = []
+    for r in range(p):
+        x = torch.empty(m, dtype=torch.bfloat16, device="cuda")
+        for s in range(0, m, 1 << 28):  # small integers: exact in bf16 under any fold order
+            e = min(m, s + (1 << 28))
+            x[s:e] = ((torch.arange(s, e, device="cuda") % 61 - 30) * (r + 1)).to(torch.bfloat16)
+        ins.append(x)
+    rs = {"direct": pkg.direct_reduce_scatter, "ring": pkg.ring_reduce_scatter,
+          "recursive": pkg.rechalf_reduce_scatter}[algo]
+    outs = [torch.empty(m // p, dtype=torch.bfloat16, device="cuda") for _ in range(p)]
+    pkg.run_ranks(p, lambda c: rs(c, ins[c.rank], out=outs[c.rank]))
+    k = m // p
+    for r in range(p):
+        for s in range(0, k, 1 << 28):
+            e = min(k, s + (1 << 28))
+            want = ((torch.arange(r * k + s, r * k + e, device="cuda") % 61 - 30) * 3).to(torch.bfloat16)
+            assert torch.equal(outs[r][s:e], want), (algo, r, s)
+    del ins, outs
+    torch.cuda.empty_cache()
