@@ -104,8 +104,11 @@ int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
 /* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "threads" (per
  * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
- * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push), "tma_stages",
- * "tma_tile", "timeout_ms", "trace". Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
+ * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL), "tma_stages",
+ * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
+ * collectives use the LL protocol — flags inside 16-byte data words, no
+ * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
+ * (group size - 1), 0 off). Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
 int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
 /* With param "trace" = 1, every launch records per-CTA events (globaltimer ns

@@ -34,7 +34,16 @@
 #define PCCL_CTRL_OFF (3 * PCCL_MAXR * PCCL_MAX_CTAS)
 #define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
-#define PCCL_FLAG_BYTES ((size_t)PCCL_NSLOTS * PCCL_SLOT_BYTES)
+// After the slots: world-level control words, then the LL (low-latency)
+// message regions (see "LL protocol" below). Both live in segment 0, so every
+// peer already has them mapped.
+#define PCCL_WCTRL_OFF ((size_t)PCCL_NSLOTS * PCCL_SLOT_WORDS)  // words: [q] LL messages exchanged with world rank q
+#define PCCL_WCTRL_WORDS 64
+#define PCCL_LL_OFF (PCCL_WCTRL_OFF + PCCL_WCTRL_WORDS)  // words
+#define PCCL_LL_HDR_BYTES 256
+#define PCCL_LL_MAX_PAYLOAD ((size_t)1 << 20)  // payload bytes per (src -> dst) message
+#define PCCL_LL_REGION_BYTES (PCCL_LL_HDR_BYTES + 2 * PCCL_LL_MAX_PAYLOAD)
+#define PCCL_FLAG_BYTES (PCCL_LL_OFF * 8 + (size_t)2 * PCCL_MAXR * PCCL_LL_REGION_BYTES)
 #define PCCL_ABORT_BIT (1ull << 63)
 
 namespace pccl {
@@ -117,6 +126,7 @@ struct Ctx {
   uint64_t t0;
   uint64_t *tr;  // trace cursor base (nullptr: tracing off)
   int ntr;
+  uint32_t ll_peers;  // LL kernels: world ranks whose channel counter the last CTA advances
 
   __device__ __forceinline__ int world(int m) const { return P->gmem[y][m]; }
   __device__ __forceinline__ uint64_t *slot_in(int m) const {
@@ -151,6 +161,7 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.t0 = global_timer_ns();
   c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
   c.ntr = 0;
+  c.ll_peers = 0;
   if (c.tr && threadIdx.x == 0) c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
   return c;
 }
@@ -167,6 +178,11 @@ struct CtaEpilogue {
       if (old == (unsigned long long)(c.P->ctas - 1)) {
         ctrl[1] = 0;
         *reinterpret_cast<volatile unsigned long long *>(ctrl) = c.epoch;
+        if (c.ll_peers) {
+          volatile uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
+          for (int q = 0; q < PCCL_MAXR; ++q)
+            if ((c.ll_peers >> q) & 1u) lc[q] = lc[q] + 1;
+        }
       }
     }
   }
@@ -357,6 +373,104 @@ __device__ __forceinline__ bool cta_exit(Ctx &c, uint32_t to, uint32_t from) {
   }
   trace_ev(c, TR_END, 0);
   return true;
+}
+
+// --------------------------------------------------------------------------
+// LL protocol (small direct collectives): flags travel inside the data.
+// Every 16-byte store carries 8 payload bytes and two copies of a 32-bit tag,
+// {d0, tag, d1, tag}; each 8-byte half is single-copy atomic over NVLink, so a
+// reader that sees both tags equal to the expected value holds valid payload.
+// A (src -> dst) channel alternates two message regions in dst's arena by the
+// parity of its message count (kept per peer in each rank's WCTRL words, and
+// advanced by the last CTA of every LL launch). Direct collectives are
+// all-to-all, so src starts message s+2 only after a collective in which dst
+// sent to src after dst had consumed message s: a region is never rewritten
+// before it was read. No entry handshake, no fence, no exit barrier; user
+// buffers are only touched locally. A 16-byte header {hash, tag, hash, tag}
+// per message carries the call signature (cross-rank mismatch -> LengthMismatch).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ char *ll_region(const LaunchParams &P, int dst, uint32_t tag, int src) {
+  return reinterpret_cast<char *>(P.flags[dst] + PCCL_LL_OFF) +
+         ((size_t)(tag & 1u) * PCCL_MAXR + src) * PCCL_LL_REGION_BYTES;
+}
+__device__ __forceinline__ void ll_st(uint4 *p, uint32_t a, uint32_t b, uint32_t tag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(tag), "r"(b), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ll_ld(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ bool ll_ok(const uint4 &v, uint32_t tag) { return v.y == tag && v.w == tag; }
+// Spin until both tags match. Returns 0, or an error code: the world error,
+// 5 on timeout, 4 when the sender's header shows another call signature
+// (checked on the slow path only, so a mismatched count cannot hang us).
+__device__ __forceinline__ int ll_wait(const Ctx &c, const uint4 *p, uint32_t tag, uint4 &v, const uint4 *hdr) {
+  uint32_t it = 0;
+  while (true) {
+    v = ll_ld(p);
+    if (ll_ok(v, tag)) return 0;
+    if ((++it & 1023u) == 0) {
+      if (*c.P->err != 0) return *c.P->err;
+      const uint4 h = ll_ld(hdr);
+      if (ll_ok(h, tag) && (h.x != c.P->meta[c.y] || h.z != c.P->meta[c.y])) return 4;
+      if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;
+    }
+  }
+}
+// Per group member m: the tag of this launch's message on channel (me, m).
+__device__ __forceinline__ void ll_tags(Ctx &c, uint32_t *s_tag) {
+  volatile const uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
+  if (threadIdx.x < c.gs) {
+    const uint64_t n = lc[c.world(threadIdx.x)] + 1;
+    s_tag[threadIdx.x] = (uint32_t)n ? (uint32_t)n : 1u;  // never 0 (cleared memory)
+  }
+  for (int m = 0; m < c.gs; ++m)
+    if (m != c.gi) c.ll_peers |= 1u << c.world(m);
+  __syncthreads();
+}
+// CTA 0: post the signature header of my message to every member.
+__device__ __forceinline__ void ll_post_headers(const Ctx &c, const uint32_t *s_tag) {
+  const int m = threadIdx.x;
+  if (c.b == 0 && m < c.gs && m != c.gi) {
+    const uint32_t meta = c.P->meta[c.y];
+    ll_st(reinterpret_cast<uint4 *>(ll_region(*c.P, c.world(m), s_tag[m], c.r)), meta, meta, s_tag[m]);
+  }
+}
+// CTA-wide, after the data: every member's header carries my signature.
+// `code` is this thread's error from the data phase (0 if none).
+__device__ __forceinline__ bool ll_finish(Ctx &c, const uint32_t *s_tag, int code) {
+  const int m = threadIdx.x;
+  if (code == 0 && m < c.gs && m != c.gi) {
+    uint4 v;
+    const uint4 *h = reinterpret_cast<const uint4 *>(ll_region(*c.P, c.r, s_tag[m], c.world(m)));
+    code = ll_wait(c, h, s_tag[m], v, h);
+    if (code == 0 && (v.x != c.P->meta[c.y] || v.z != c.P->meta[c.y])) code = 4;
+    if (code == 4 && atomicCAS((int *)&c.P->err[8], 0, 1) == 0) {
+      c.P->err[9] = (int)c.epoch;
+      c.P->err[10] = (int)(c.P->meta[c.y] & 0x3fffffu);
+      c.P->err[11] = (int)(v.x & 0x3fffffu);
+      c.P->err[12] = c.r;
+      c.P->err[13] = -1;
+      c.P->err[14] = c.world(m);
+      c.P->err[15] = c.b;
+    }
+  }
+  if (__syncthreads_and(code == 0)) {
+    trace_ev(c, TR_END, 0);
+    return true;
+  }
+  __shared__ int s_code;
+  if (threadIdx.x == 0) s_code = 0;
+  __syncthreads();
+  if (code != 0) atomicCAS(&s_code, 0, code);
+  __syncthreads();
+  abort_group(c, s_code ? s_code : 5);
+  return false;
 }
 
 // --------------------------------------------------------------------------

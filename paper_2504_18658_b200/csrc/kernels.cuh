@@ -616,6 +616,189 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
 
 
 // ============================================================================
+// LL direct collectives (small messages; protocol in device.cuh)
+// ============================================================================
+// Payload unit = 8 bytes (P.blk etc. are in 8-byte units). Every CTA owns
+// units [lo,hi) of each (sub-)block: it posts them to every peer, then reads
+// the peers' words of the same range — all peers' loads issued before any is
+// waited on — and writes them out locally.
+template <int MAXP>
+__global__ void __launch_bounds__(kThreads) k_ag_direct_ll(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  __shared__ uint32_t s_tag[PCCL_MAXR];
+  ll_tags(c, s_tag);
+  const int gs = c.gs, gi = c.gi, nt = blockDim.x;
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  ll_post_headers(c, s_tag);
+  for (int t = 0; t < P.nsubblk; ++t) {
+    const uint2 *src = reinterpret_cast<const uint2 *>(P.send[c.r]) + (int64_t)t * P.send_sub_stride;
+    uint2 *mine = reinterpret_cast<uint2 *>(ag_block<8>(P, P.recv[c.r], c.y, gi, t));
+    for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
+      const uint2 v = __ldg(src + e);
+#pragma unroll
+      for (int i = 1; i < MAXP; ++i) {
+        if (i >= gs) break;
+        const int q = (gi + i) % gs;
+        uint4 *d = reinterpret_cast<uint4 *>(ll_region(P, c.world(q), s_tag[q], c.r) + PCCL_LL_HDR_BYTES);
+        ll_st(d + (int64_t)t * P.blk + e, v.x, v.y, s_tag[q]);
+      }
+      if (P.local_copy) mine[e] = v;
+    }
+  }
+  int code = 0;
+  for (int t = 0; t < P.nsubblk && !code; ++t) {
+    for (int64_t e = lo + threadIdx.x; e < hi && !code; e += nt) {
+      uint4 v[MAXP];
+#pragma unroll
+      for (int i = 1; i < MAXP; ++i) {
+        if (i < gs) {
+          const int q = (gi + gs - i) % gs;
+          v[i] = ll_ld(reinterpret_cast<const uint4 *>(ll_region(P, c.r, s_tag[q], c.world(q)) + PCCL_LL_HDR_BYTES) +
+                       (int64_t)t * P.blk + e);
+        }
+      }
+#pragma unroll
+      for (int i = 1; i < MAXP; ++i) {
+        if (i < gs && !code) {
+          const int q = (gi + gs - i) % gs;
+          const char *reg = ll_region(P, c.r, s_tag[q], c.world(q));
+          if (!ll_ok(v[i], s_tag[q]))
+            code = ll_wait(c, reinterpret_cast<const uint4 *>(reg + PCCL_LL_HDR_BYTES) + (int64_t)t * P.blk + e,
+                           s_tag[q], v[i], reinterpret_cast<const uint4 *>(reg));
+          reinterpret_cast<uint2 *>(ag_block<8>(P, P.recv[c.r], c.y, q, t))[e] = make_uint2(v[i].x, v[i].z);
+        }
+      }
+    }
+  }
+  ll_finish(c, s_tag, code);
+}
+
+// 8 payload bytes as N accumulator lanes
+template <int DT> struct LLU;
+template <> struct LLU<DT_F32> {
+  static constexpr int N = 2;
+  struct Acc { float v[2]; };
+  static __device__ __forceinline__ Acc load(uint2 u) { Acc a; a.v[0] = __uint_as_float(u.x); a.v[1] = __uint_as_float(u.y); return a; }
+  static __device__ __forceinline__ uint2 store(const Acc &a) { return make_uint2(__float_as_uint(a.v[0]), __float_as_uint(a.v[1])); }
+};
+template <> struct LLU<DT_BF16> {
+  static constexpr int N = 4;
+  struct Acc { float v[4]; };
+  static __device__ __forceinline__ Acc load(uint2 u) {
+    Acc a; float2 f = bf2_to_f2(u.x); a.v[0] = f.x; a.v[1] = f.y; f = bf2_to_f2(u.y); a.v[2] = f.x; a.v[3] = f.y; return a;
+  }
+  static __device__ __forceinline__ uint2 store(const Acc &a) {
+    return make_uint2(f2_to_bf2(a.v[0], a.v[1]), f2_to_bf2(a.v[2], a.v[3]));
+  }
+};
+template <> struct LLU<DT_F16> {
+  static constexpr int N = 4;
+  struct Acc { float v[4]; };
+  static __device__ __forceinline__ Acc load(uint2 u) {
+    Acc a; float2 f = h2_to_f2(u.x); a.v[0] = f.x; a.v[1] = f.y; f = h2_to_f2(u.y); a.v[2] = f.x; a.v[3] = f.y; return a;
+  }
+  static __device__ __forceinline__ uint2 store(const Acc &a) {
+    return make_uint2(f2_to_h2(a.v[0], a.v[1]), f2_to_h2(a.v[2], a.v[3]));
+  }
+};
+
+// Chunk q of my input goes to member q as an LL message; my output chunk is
+// folded from my own chunk and the p-1 received ones in the named order
+// (same folds as k_rs_direct, so results are bit-identical to it).
+template <int DT, int ORDER, int MAXP>
+__global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant__ LaunchParams P) {
+  using R = LLU<DT>;
+  using Acc = typename R::Acc;
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  __shared__ uint32_t s_tag[PCCL_MAXR];
+  ll_tags(c, s_tag);
+  const int gs = c.gs, gi = c.gi, nt = blockDim.x;
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  const uint2 *own = reinterpret_cast<const uint2 *>(P.send[c.r]) + P.base[c.y];
+  ll_post_headers(c, s_tag);
+  for (int i = 1; i < gs; ++i) {
+    const int q = (gi + i) % gs;
+    uint4 *d = reinterpret_cast<uint4 *>(ll_region(P, c.world(q), s_tag[q], c.r) + PCCL_LL_HDR_BYTES);
+    for (int j = 0; j < P.nsubblk; ++j) {
+      const uint2 *src = own + (int64_t)q * P.istride + (int64_t)j * P.sub_stride;
+      for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
+        const uint2 v = __ldg(src + e);
+        ll_st(d + (int64_t)j * P.blk + e, v.x, v.y, s_tag[q]);
+      }
+    }
+  }
+  int code = 0;
+  for (int j = 0; j < P.nsubblk && !code; ++j) {
+    uint2 *dst = reinterpret_cast<uint2 *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
+    const uint2 *mine = own + (int64_t)gi * P.istride + (int64_t)j * P.sub_stride;
+    for (int64_t e = lo + threadIdx.x; e < hi && !code; e += nt) {
+      uint4 w[MAXP];
+      int qs[MAXP];
+#pragma unroll
+      for (int i = 0; i < MAXP; ++i) {
+        int q;
+        if (ORDER == O_RING) q = (gi + 1 + i) % gs;
+        else if (ORDER == O_REC) q = gi ^ i;
+        else q = i;
+        qs[i] = q;
+        if (i < gs && q != gi)
+          w[i] = ll_ld(reinterpret_cast<const uint4 *>(ll_region(P, c.r, s_tag[q], c.world(q)) + PCCL_LL_HDR_BYTES) +
+                       (int64_t)j * P.blk + e);
+      }
+      uint2 raw[MAXP];
+#pragma unroll
+      for (int i = 0; i < MAXP; ++i) {
+        const int q = qs[i];
+        raw[i] = make_uint2(0u, 0u);
+        if (i >= gs) continue;
+        if (q == gi) {
+          raw[i] = __ldg(mine + e);
+        } else {
+          if (!ll_ok(w[i], s_tag[q]) && !code) {
+            const char *reg = ll_region(P, c.r, s_tag[q], c.world(q));
+            code = ll_wait(c, reinterpret_cast<const uint4 *>(reg + PCCL_LL_HDR_BYTES) + (int64_t)j * P.blk + e, s_tag[q],
+                           w[i], reinterpret_cast<const uint4 *>(reg));
+          }
+          raw[i] = make_uint2(w[i].x, w[i].z);
+        }
+      }
+      if (code) break;
+      Acc acc;
+      if (ORDER == O_REC) {
+        Acc v[MAXP];
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
+#pragma unroll
+        for (int h = MAXP / 2; h >= 1; h >>= 1) {
+          if (h < gs) {
+#pragma unroll
+            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+          }
+        }
+        acc = v[0];
+      } else if (ORDER == O_RANK) {
+#pragma unroll
+        for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      } else {
+        acc = R::load(raw[0]);
+#pragma unroll
+        for (int i = 1; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      }
+      dst[e] = R::store(acc);
+    }
+  }
+  ll_finish(c, s_tag, code);
+}
+
+// ============================================================================
 // raw NVLink probe (debug): every CTA streams 16-byte vectors to (push) or
 // from (pull) the peers in dst_mask, round-robin by CTA; no flags, no order.
 // ============================================================================

@@ -53,6 +53,7 @@ struct pccl_world {
   int poisoned = 0;  // sticky device error
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
+  int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
   uint32_t meta_skew[PCCL_MAXR] = {};
@@ -184,6 +185,30 @@ KernelFn rs_kernel_dt(int algo, int order, int maxp, int variant) {
   return variant == 1 ? rs_direct_kernel<DT, VEC, true>(order, maxp) : rs_direct_kernel<DT, VEC, false>(order, maxp);
 }
 
+template <int DT>
+KernelFn rs_ll_dt(int order, int maxp) {
+#define RLL(O)                                                  \
+  if (order == O) {                                             \
+    switch (maxp) {                                             \
+      case 2: return (KernelFn)k_rs_direct_ll<DT, O, 2>;        \
+      case 4: return (KernelFn)k_rs_direct_ll<DT, O, 4>;        \
+      case 8: return (KernelFn)k_rs_direct_ll<DT, O, 8>;        \
+      default: return (KernelFn)k_rs_direct_ll<DT, O, 16>;      \
+    }                                                           \
+  }
+  RLL(O_RING)
+  RLL(O_REC)
+  RLL(O_RANK)
+#undef RLL
+  return nullptr;
+}
+KernelFn rs_ll_kernel(int dt, int order, int maxp) {
+  if (dt == PCCL_FLOAT32) return rs_ll_dt<DT_F32>(order, maxp);
+  if (dt == PCCL_BFLOAT16) return rs_ll_dt<DT_BF16>(order, maxp);
+  if (dt == PCCL_FLOAT16) return rs_ll_dt<DT_F16>(order, maxp);
+  return nullptr;
+}
+
 KernelFn rs_kernel(int dt, bool vec, int algo, int order, int maxp, int variant) {
 #define RSK(D)                                                                                              \
   return vec ? rs_kernel_dt<D, true>(algo, order, maxp, variant) : rs_kernel_dt<D, false>(algo, order, maxp, variant);
@@ -252,7 +277,21 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   int U;  // bytes per unit
   KernelFn k;
   size_t smem = 0;
-  if (pl.coll == PCCL_ALL_GATHER) {
+  if (pl.variant == 4) {  // LL protocol: 8-byte payload units (host checked the alignment)
+    U = 8;
+    int maxp = 2;
+    while (maxp < pl.gs) maxp <<= 1;
+    if (pl.coll == PCCL_ALL_GATHER) {
+      switch (maxp) {
+        case 2: k = (KernelFn)k_ag_direct_ll<2>; break;
+        case 4: k = (KernelFn)k_ag_direct_ll<4>; break;
+        case 8: k = (KernelFn)k_ag_direct_ll<8>; break;
+        default: k = (KernelFn)k_ag_direct_ll<16>; break;
+      }
+    } else {
+      k = rs_ll_kernel(pl.dtype, pl.order, maxp);
+    }
+  } else if (pl.coll == PCCL_ALL_GATHER) {
     U = 16;
     while (U > 1 && (acc & (uint64_t)(U - 1))) U >>= 1;
     if ((size_t)U < es && es <= 16 && !(acc & (es - 1))) U = (int)es;
@@ -340,6 +379,10 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     // wants ~one CTA per SM.
     const double S = (double)pl.gs * (double)pl.count * (double)es;
     ctas = w->emu ? PCCL_MAX_CTAS : (S >= 16.0 * (1 << 20) ? 128 : S >= 4.0 * (1 << 20) ? 64 : 48);
+    if (pl.variant == 4) {  // LL: about one 8-byte unit per thread and peer
+      const int64_t u = P.blk * (int64_t)pl.nsubblk;
+      ctas = (int)std::max<int64_t>(1, std::min<int64_t>(w->emu ? PCCL_MAX_CTAS : 64, (u + threads - 1) / threads));
+    }
   }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
   {
@@ -447,6 +490,39 @@ struct Binder {
   }
 };
 
+// LL protocol choice (device.cuh): small direct collectives whose per-peer
+// message fits an LL region. Depends only on SPMD-uniform values (size,
+// world parameters), never on this rank's pointers, so all members agree.
+// Auto threshold (tools/latency.py, p=2/4, graph-replayed, r1): LL beats the
+// flag protocol until a rank's total LL egress reaches ~0.75-1 MiB (p=2: 9.4
+// vs 11.2 us at 1 MiB per peer; p=4: tie at 256 KiB per peer).
+constexpr size_t kLLEgress = 768u << 10;
+bool use_ll(const pccl_world *w, int64_t variant_param, size_t msg_bytes, int gs) {
+  if (variant_param != -1 && variant_param != 4) return false;
+  size_t cap = PCCL_LL_MAX_PAYLOAD;
+  if (variant_param != 4) {
+    const size_t lim = w->p_ll_max < 0 ? kLLEgress / (size_t)std::max(1, gs - 1) : (size_t)w->p_ll_max;
+    cap = std::min(cap, lim);
+  }
+  return gs <= PCCL_MAXR && msg_bytes > 0 && msg_bytes % 8 == 0 && msg_bytes <= cap;
+}
+
+// LL kernels touch user buffers only locally, with 8-byte accesses: a
+// misaligned buffer on this rank is bounced through local staging.
+bool ll_local(Binder &B, int r, char *&p, size_t bytes, bool copy_in, std::vector<std::pair<char *, char *>> *out) {
+  if (((uintptr_t)p & 7u) == 0) return true;
+  size_t off;
+  char *s = B.stage(r, bytes, &off);
+  if (!s) return false;
+  if (copy_in && cudaMemcpyAsync(s, p, bytes, cudaMemcpyDeviceToDevice, B.stream) != cudaSuccess) {
+    B.status = PCCL_ERR_CUDA;
+    return false;
+  }
+  if (out) out->push_back({s, p});
+  p = s;
+  return true;
+}
+
 // A device-reported error poisons the world: kernels that aborted did not
 // finish their protocol, so every later call fails fast with the same code
 // until pccl_world_reset_flags (emulation) or the world is recreated.
@@ -485,6 +561,32 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.blk = (int64_t)count;
   pl.istride = (int64_t)count;
   pl.send_sub_stride = (int64_t)count;
+  if (algo == A_DIRECT && use_ll(w, w->p_ag_variant, blk_bytes, gs)) {
+    pl.variant = 4;
+    Binder B{w, stream};
+    std::vector<std::pair<char *, char *>> copy_out;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i];
+      int gi = -1;
+      for (int m = 0; m < gs; ++m)
+        if (c->members[m] == r) gi = m;
+      if (gi < 0) return PCCL_ERR_INDEX_OUT_OF_RANGE;
+      pl.rows.push_back({r, c});
+      B.cursor = 0;
+      char *snd = (char *)sends[i], *rcv = (char *)recvs[i];
+      const bool inplace = snd == rcv + (size_t)gi * blk_bytes;
+      if (!ll_local(B, r, rcv, gs * blk_bytes, false, &copy_out)) return B.status;
+      if (inplace) snd = rcv + (size_t)gi * blk_bytes;
+      if (!ll_local(B, r, snd, blk_bytes, true, nullptr)) return B.status;
+      pl.send[r] = snd;
+      pl.recv[r] = rcv;
+      pl.local_copy = snd != rcv + (size_t)gi * blk_bytes;
+    }
+    int s = launch(w, pl, stream);
+    if (s) return s;
+    for (auto &co : copy_out) CK(cudaMemcpyAsync(co.second, co.first, gs * blk_bytes, cudaMemcpyDeviceToDevice, stream));
+    return PCCL_SUCCESS;
+  }
   {
     // Data movement. auto: push (posted NVLink stores, saturates the links
     // with few SMs) whenever the output is symmetric; a direct all-gather into
@@ -564,6 +666,28 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.blk = (int64_t)recvcount;
   pl.istride = (int64_t)recvcount;
   pl.out_sub_stride = (int64_t)recvcount;
+  if (algo == A_DIRECT && use_ll(w, w->p_rs_variant, chunk_bytes, gs)) {
+    pl.variant = 4;
+    Binder B{w, stream};
+    std::vector<std::pair<char *, char *>> copy_out;
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      const int r = ranks[i];
+      bool member = false;
+      for (int m = 0; m < gs; ++m) member |= c->members[m] == r;
+      if (!member) return PCCL_ERR_INDEX_OUT_OF_RANGE;
+      pl.rows.push_back({r, c});
+      B.cursor = 0;
+      char *snd = (char *)sends[i], *rcv = (char *)recvs[i];
+      if (!ll_local(B, r, snd, gs * chunk_bytes, true, nullptr)) return B.status;
+      if (!ll_local(B, r, rcv, chunk_bytes, false, &copy_out)) return B.status;
+      pl.send[r] = snd;
+      pl.out[r] = rcv;
+    }
+    int s = launch(w, pl, stream);
+    if (s) return s;
+    for (auto &co : copy_out) CK(cudaMemcpyAsync(co.second, co.first, chunk_bytes, cudaMemcpyDeviceToDevice, stream));
+    return PCCL_SUCCESS;
+  }
   {
     // auto: pull (peer loads fused with the add, no staging hop) for direct /
     // recursive halving when the input is symmetric; push for ring, and for
@@ -825,6 +949,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_NSUB")) w->p_nsub = atoi(t);
   if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
   if (const char *t = getenv("PCCL_LOCAL_FENCE")) w->p_local_fence = atoi(t);
+  if (const char *t = getenv("PCCL_LL_MAX")) w->p_ll_max = atoll(t);
   if (const char *t = getenv("PCCL_PDL")) w->p_pdl = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
   if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
@@ -920,6 +1045,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "trace")) return &w->p_trace;
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
+  if (!strcmp(key, "ll_max")) return &w->p_ll_max;
   return nullptr;
 }
 
@@ -1053,7 +1179,7 @@ size_t pccl_staging_bytes(int collective, int algo, int gs, size_t count, int dt
   const size_t full = align256((size_t)gs * count * es), blk = align256(count * es);
   if (collective == PCCL_ALL_GATHER) return full + blk;
   if (algo == 3) return 4 * full;
-  return algo == A_DIRECT ? full : 2 * full;
+  return algo == A_DIRECT ? full + blk : 2 * full;  // direct LL may bounce a misaligned input and output
 }
 
 int pccl_comm_create(pccl_world_t w, const int *members, int n, int comm_id, pccl_comm_t *out) {

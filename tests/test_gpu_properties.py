@@ -230,9 +230,11 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
     sp = _lib.ptr_array([t.data_ptr() for t in ins])
     rp = _lib.ptr_array([t.data_ptr() for t in outs])
     steps = len(_lib.schedule(1 if coll == "rs" else 0, a, 1, 1, p, n * p * 4))
+    ll_max = w.get_param("ll_max")
     try:
         w.set_param("trace", 1)
         w.set_param("nsub", 1)
+        w.set_param("ll_max", 0)  # the bulk (flag) protocol: LL has no per-step waits
         s = torch.cuda.current_stream().cuda_stream
         if coll == "rs":
             _lib.check(L.pccl_emu_reduce_scatter(group.handle, a, 0, sp, rp, n, 0, s))
@@ -242,6 +244,7 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
         tr = w.trace()
     finally:
         w.set_param("trace", 0)
+        w.set_param("ll_max", ll_max)
     assert len(tr) == p
     # default data movement for symmetric buffers: AG push; RS ring push,
     # recursive / direct pull. Waits per CTA = the algorithm's steps plus the
@@ -298,3 +301,101 @@ def test_offsets_beyond_4gib(algo):
             assert torch.equal(outs[r][s:e], want), (algo, r, s)
     del ins, outs
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------------------
+# LL protocol (small direct collectives): same results as the bulk path and
+# the oracle; channel parity across groups; misaligned buffers
+# ---------------------------------------------------------------------------
+def _with_ll(world, value, fn):
+    old = world.get_param("ll_max")
+    world.set_param("ll_max", value)
+    try:
+        return fn()
+    finally:
+        world.set_param("ll_max", old)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8, 16])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_ll_direct_matches_bulk_and_oracle(p, dtype):
+    pkg = _pkg()
+    world = pkg.emulated_world(p)
+    rng = np.random.default_rng(p * 7 + len(dtype))
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[dtype]
+    per8 = {"f32": 2, "bf16": 4, "f16": 4}[dtype]
+    for n in (per8, per8 * 3, per8 * 1000, (64 << 10) // (8 // per8)):
+        xs = [torch.from_numpy(rng.standard_normal(n * p).astype(np.float32)).to(tdt).cuda() for _ in range(p)]
+        orders = ["ring", "rank"] + (["recursive"] if p & (p - 1) == 0 else [])
+        for order in orders:
+            run = lambda: pkg.run_ranks(p, lambda c: pkg.direct_reduce_scatter(c, xs[c.rank], order=order).cpu())  # noqa: E731
+            ll = _with_ll(world, 1 << 20, run)
+            bulk = _with_ll(world, 0, run)
+            if dtype != "f16":
+                want = oracle.direct_reduce_scatter([_dev_np(x.cpu(), dtype) for x in xs], dtype if dtype == "bf16" else "f32",
+                                                    order)
+            for r in range(p):
+                assert torch.equal(ll[r].view(torch.int16 if tdt != torch.float32 else torch.int32),
+                                   bulk[r].view(torch.int16 if tdt != torch.float32 else torch.int32)), (order, r, n)
+                if dtype != "f16":
+                    assert np.array_equal(_dev_np(ll[r], dtype).view(np.uint8), np.asarray(want[r]).view(np.uint8))
+        ag = lambda: pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, xs[c.rank][:n]).cpu())  # noqa: E731
+        ll = _with_ll(world, 1 << 20, ag)
+        want = torch.cat([x[:n].cpu() for x in xs])
+        for r in range(p):
+            assert torch.equal(ll[r], want)
+
+
+def test_ll_channels_alternate_across_groups_and_protocols():
+    """Back-to-back LL calls on the world and on overlapping sub-groups,
+    interleaved with bulk calls: each channel's two regions alternate by its
+    own message count, so every result stays exact."""
+    pkg = _pkg()
+    p, n = 4, 512
+
+    def body(c):
+        lo = c.subgroup([0, 1], 1) if c.rank < 2 else c.subgroup([2, 3], 2)
+        odd = c.subgroup([1, 2, 3], 3) if c.rank > 0 else None
+        bad = []
+        for it in range(40):
+            x = torch.full((n * p,), float(it * 10 + c.rank + 1), device="cuda")
+            y = pkg.direct_reduce_scatter(c, x)
+            if float(y[0]) != sum(it * 10 + q + 1 for q in range(p)):
+                bad.append(("world_rs", it))
+            z = pkg.direct_all_gather(lo, x[:n])
+            if [float(z[0]), float(z[-1])] != [float(it * 10 + lo.members[0] + 1), float(it * 10 + lo.members[1] + 1)]:
+                bad.append(("pair_ag", it))
+            if odd is not None and it % 3 == 0:
+                w = pkg.direct_all_gather(odd, x[:n])
+                if float(w[-1]) != float(it * 10 + 4):
+                    bad.append(("odd_ag", it))
+            if it % 5 == 0:  # bulk protocol in between (4 MiB)
+                big = torch.full(((1 << 20) * p,), 1.0, device="cuda")
+                if float(pkg.reduce_scatter(c, big, algorithm="direct")[0]) != p:
+                    bad.append(("bulk", it))
+        torch.cuda.synchronize()
+        return bad
+
+    outs = pkg.run_ranks(p, body)
+    assert outs == [[]] * p
+
+
+def test_ll_misaligned_buffers_are_bounced():
+    pkg = _pkg()
+    p, n = 4, 1000
+    base = [torch.arange(n * p + 1, dtype=torch.float32, device="cuda") * (r + 1) for r in range(p)]
+    xs = [b[1:] for b in base]  # 4-byte offset: not 8-byte aligned
+    assert xs[0].data_ptr() % 8 == 4
+    outs_raw = [torch.zeros(n + 1, device="cuda") for _ in range(p)]
+    outs = [o[1:] for o in outs_raw]
+    pkg.run_ranks(p, lambda c: pkg.direct_reduce_scatter(c, xs[c.rank], out=outs[c.rank]))
+    total = sum(range(1, p + 1))
+    for r in range(p):
+        want = (torch.arange(n * p + 1, dtype=torch.float32)[1:] * total)[r * n:(r + 1) * n]
+        assert torch.equal(outs[r].cpu(), want)
+    ag_raw = [torch.zeros(n * p + 1, device="cuda") for _ in range(p)]
+    ags = [a[1:] for a in ag_raw]
+    pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, xs[c.rank][:n], out=ags[c.rank]))
+    want = torch.cat([x[:n].cpu() for x in xs])
+    for r in range(p):
+        assert torch.equal(ags[r].cpu(), want)

@@ -12,6 +12,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--coll", default="rs_bf16"); ap.add_argument("--algo", default="recursive")
     ap.add_argument("--variant", type=int, default=-1); ap.add_argument("--size-mib", type=int, default=128)
+    ap.add_argument("--size-kib", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0); ap.add_argument("--nsub", type=int, default=1)
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -21,7 +22,7 @@ def main():
     from paper_2504_18658_b200 import _lib
     comm = pkg.init_from_torch(device=dev.index); w = comm.world; L = _lib.lib()
     kind, dt = a.coll.split("_"); dtype = torch.bfloat16 if dt == "bf16" else torch.float32
-    es = 2 if dt == "bf16" else 4; code = _lib.DTYPES[dt]; S = a.size_mib << 20; n = S // es // p
+    es = 2 if dt == "bf16" else 4; code = _lib.DTYPES[dt]; S = (a.size_kib << 10) if a.size_kib else (a.size_mib << 20); n = S // es // p
     sin = w.empty(n * p if kind == "rs" else n, dtype); sout = w.empty(n if kind == "rs" else n * p, dtype); sin.normal_()
     alg = _lib.ALGOS[a.algo]
     w.ensure_staging(int(L.pccl_staging_bytes(1 if kind == "rs" else 0, alg, p, n, code)))
@@ -56,7 +57,7 @@ def main():
     outs = [None] * p
     dist.all_gather_object(outs, "\n".join(out))
     if rank == 0:
-        print(f"== {a.coll} {a.algo} variant={a.variant} p={p} {a.size_mib} MiB ctas={a.ctas or 'auto'} nsub={a.nsub}")
+        print(f"== {a.coll} {a.algo} variant={a.variant} p={p} {S >> 10} KiB ctas={a.ctas or 'auto'} nsub={a.nsub}")
         for o in outs[:2]: print(o)
     dist.barrier(); dist.destroy_process_group()
 
