@@ -53,8 +53,20 @@ def _align(n: int) -> int:
     return (n + 255) & ~255
 
 
+try:  # raw handle of the current stream without building a Stream object
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover
+    _raw_stream = None
+
+
 def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def _stream_of(t: torch.Tensor) -> int:
+    if _raw_stream is not None:
+        return _raw_stream(t.get_device())
+    return torch.cuda.current_stream(t.device).cuda_stream
 
 
 # ---------------------------------------------------------------------------
@@ -194,8 +206,69 @@ def _upload(comm, args: list, ranks: list, out_bytes: int):
     return sends, recvs
 
 
+_REDUCE_DTYPES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+
+
+def _fast_device(comm, buf, reduce: bool, algo: str, order: str, out):
+    """Real mode with contiguous CUDA tensors: validate and go straight to the
+    C ABI (stream-ordered, no host sync, ~7 us of host time per call instead
+    of ~20). Returns None when the general path must handle the call."""
+    if comm.emulated or type(buf) is not torch.Tensor or not buf.is_cuda or not buf.is_contiguous():
+        return None
+    if reduce:
+        code = _REDUCE_DTYPES.get(buf.dtype)
+    else:
+        name = TORCH_DTYPES.get(buf.dtype)
+        code = None if name is None else _lib.DTYPES[name]
+    if code is None or (out is not None and (type(out) is not torch.Tensor or not out.is_cuda
+                                             or not out.is_contiguous() or out.dtype != buf.dtype)):
+        return None
+    p = comm.size
+    n = buf.numel()
+    pow2 = p & (p - 1) == 0
+    if reduce:
+        if n % p:
+            raise NotDivisible(f"input of {n} elements not divisible by p={p}")
+        if (algo == "recursive" or (algo == "direct" and order == "recursive")) and not pow2:
+            raise NonPowerOfTwo(f"recursive algorithms require power-of-two ranks, got {p}")
+        cnt = n // p
+        out_numel = cnt
+    else:
+        if algo == "recursive" and not pow2:
+            raise NonPowerOfTwo(f"recursive doubling requires power-of-two ranks, got {p}")
+        cnt = n
+        out_numel = n * p
+    if out is None:
+        out = torch.empty(out_numel, dtype=buf.dtype, device=buf.device)
+    elif out.numel() != out_numel:
+        raise LengthMismatch(f"output has {out.numel()} elements, expected {out_numel}")
+    a = _lib.ALGOS[algo]
+    comm.next_base_tag()
+    key = (reduce, a, cnt, code)
+    need = comm._stage_need.get(key)
+    if need is None:
+        need = int(lib().pccl_staging_bytes(1 if reduce else 0, a, p, cnt, code))
+        comm._stage_need[key] = need
+    st = comm.world.staging
+    if (st is None or st.nbytes < need) and _check_world_size_growth(comm, need, "staging"):
+        comm.world.ensure_staging(need)
+    stream = _stream_of(buf)
+    L = lib()
+    if reduce:
+        status = L.pccl_reduce_scatter(comm.handle, a, _lib.ORDERS[order], buf.data_ptr(), out.data_ptr(), cnt, code,
+                                       stream)
+    else:
+        status = L.pccl_all_gather(comm.handle, a, buf.data_ptr(), out.data_ptr(), cnt, code, stream)
+    if status:
+        check(status, f"{'reduce_scatter' if reduce else 'all_gather'}[{algo}]")
+    return out
+
+
 def _run(comm, buf, reduce: bool, algo: str, order: str, out=None):
     """One rank's call (real) or rendezvous into one launch (emulated)."""
+    fast = _fast_device(comm, buf, reduce, algo, order, out)
+    if fast is not None:
+        return fast
     arg = _In(buf, reduce, comm.device, out)
     p = comm.size
     if reduce:

@@ -117,6 +117,7 @@ class Communicator:
         self._group = _group or _GroupHandle(world, self.members, comm_id)
         self._rdv = _rdv
         self._next_seq = 0
+        self._stage_need: dict = {}  # (reduce, algo, count, dtype) -> staging bytes
 
     @property
     def size(self) -> int:

@@ -156,6 +156,7 @@ class FlatTable:
 
     def add(self, e: FlatEntry) -> None:
         self.entries.append(e)
+        _choice_cache.clear()
 
     def best(self, collective: str, p: int, m_bytes: float) -> str:
         cands = [e for e in self.entries if e.collective == collective and e.p == p]
@@ -192,9 +193,21 @@ def flat_table() -> FlatTable | None:
     return _flat_table
 
 
+_choice_cache: dict = {}
+
+
 def choose_algorithm(collective: str, p: int, m_bytes: float) -> str:
     """Measured winner for (collective, p, size); one-shot ``direct`` (the
-    fewest steps over a full-bandwidth switch) when nothing was measured."""
+    fewest steps over a full-bandwidth switch) when nothing was measured.
+    Memoised per (collective, p, size); table edits clear the memo."""
+    key = (collective, p, m_bytes)
+    hit = _choice_cache.get(key)
+    if hit is None:
+        hit = _choice_cache[key] = _choose(collective, p, m_bytes)
+    return hit
+
+
+def _choose(collective: str, p: int, m_bytes: float) -> str:
     t = flat_table()
     if t is not None:
         try:

@@ -76,6 +76,7 @@ def autotune(comm, collective: str, m_bytes: int, *, dtype=torch.bfloat16, algor
     finally:
         world.destroy_segment(seg)
     t = _table()
+    _sel._choice_cache.clear()
     t.entries = [e for e in t.entries if not (e.collective == collective and e.p == p and e.m_bytes == m_bytes)]
     result = {}
     for a, s in zip(algos, tmax):

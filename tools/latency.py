@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--colls", default="ag,rs")
     ap.add_argument("--pdl", default="1", help="comma list of PDL settings to compare (param pdl)")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--api", choices=["c", "python"], default="c",
+                    help="c: ctypes calls of the C ABI; python: the package's public functions")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
@@ -85,13 +87,16 @@ def main():
                 w.set_param("pdl", pdl)
                 al = _lib.ALGOS[algo]
                 w.ensure_staging(int(L.pccl_staging_bytes(0 if coll == "ag" else 1, al, p, n, 0)))
-                if coll == "ag":
+                if a.api == "python":
+                    op = pkg.all_gather if coll == "ag" else pkg.reduce_scatter
+                    fn = lambda s, op=op, algo=algo: op(comm, x, algorithm=algo, out=y)  # noqa: E731
+                elif coll == "ag":
                     fn = lambda s: _lib.check(L.pccl_all_gather(comm.handle, al, x.data_ptr(), y.data_ptr(), n, 0, s))  # noqa: E731
                 else:
                     fn = lambda s: _lib.check(L.pccl_reduce_scatter(comm.handle, al, 0, x.data_ptr(), y.data_ptr(), n, 0, s))  # noqa: E731
                 d, h, g = measure(fn, a.k)
                 if rank == 0:
-                    print(f"p={p} {coll} {S >> 10:7d} KiB {algo:10s} pdl={pdl} eager {d:7.2f} us/call (host enqueue {h:6.2f}) "
+                    print(f"p={p} {a.api:6s} {coll} {S >> 10:7d} KiB {algo:10s} pdl={pdl} eager {d:7.2f} us/call (host enqueue {h:6.2f}) "
                           f"graph {g:7.2f} us/call", flush=True)
             if a.no_nccl:
                 continue
