@@ -153,7 +153,14 @@ class Communicator:
     # -- emulation plumbing ------------------------------------------------
     def _rendezvous(self, payload, execute):
         key = (self.members, self.comm_id, self.next_base_tag())
-        return self._rdv.arrive(key, self.size, self.rank, payload, execute)
+
+        def locked(payloads):
+            # emulated sub-groups share the world's staging segment and one
+            # device: their host-side staging copies + launch must not interleave
+            with self.world.lock:
+                return execute(payloads)
+
+        return self._rdv.arrive(key, self.size, self.rank, payload, locked)
 
     def barrier(self) -> None:
         """Device-side barrier: a zero-byte all-gather (entry + exit handshake

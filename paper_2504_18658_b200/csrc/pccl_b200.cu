@@ -28,6 +28,15 @@ struct Segment {
 
 }  // namespace
 
+struct OccKey {
+  const void *k;
+  int threads;
+  size_t smem;
+  bool operator<(const OccKey &o) const {
+    return k != o.k ? k < o.k : threads != o.threads ? threads < o.threads : smem < o.smem;
+  }
+};
+
 struct pccl_world {
   int nranks = 0;
   int rank = -1;  // -1: emulation
@@ -58,6 +67,8 @@ struct pccl_world {
   int trace_rows = 0, trace_ctas = 0;
   uint32_t meta_skew[PCCL_MAXR] = {};
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
+  std::map<OccKey, int> occ_cache;              // co-resident CTAs per SM, per (kernel, threads, smem)
+  std::mutex occ_mu;
 };
 
 struct pccl_comm {
@@ -386,10 +397,22 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
   {
-    int per_sm = 0;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, threads, smem));
-    const int cap = std::max(1, per_sm) * w->sms;  // every CTA must be co-resident (they wait on each other)
+    // every CTA must be co-resident (they wait on each other); the occupancy
+    // query costs microseconds of host time, so it is cached per configuration
+    const OccKey key{(const void *)k, threads, smem};
+    int per_sm = -1;
+    {
+      std::lock_guard<std::mutex> lk(w->occ_mu);  // emulated sub-groups may launch from several threads
+      auto it = w->occ_cache.find(key);
+      if (it != w->occ_cache.end()) per_sm = it->second;
+    }
+    if (per_sm < 0) {
+      if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, threads, smem));
+      std::lock_guard<std::mutex> lk(w->occ_mu);
+      w->occ_cache[key] = per_sm;
+    }
+    const int cap = std::max(1, per_sm) * w->sms;
     ctas = std::max(1, std::min(ctas, cap / nrows));
   }
   P.ctas = ctas;
@@ -402,7 +425,6 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     w->trace_ctas = ctas;
   }
   dim3 grid(ctas, nrows), block(threads);
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (w->emu) {
     void *args[] = {&P};
     CK(cudaLaunchCooperativeKernel((const void *)k, grid, block, args, smem, stream));
@@ -592,6 +614,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
     // with few SMs) whenever the output is symmetric; a direct all-gather into
     // an unregistered output pulls instead (only the small send is staged).
     int v = (int)w->p_ag_variant;
+    if (v == 4) v = -1;  // LL requested but this message does not qualify
     if (v < 0) {
       int seg;
       size_t off;
@@ -693,6 +716,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     // recursive halving when the input is symmetric; push for ring, and for
     // every algorithm when the input is unregistered (no input staging copy).
     int v = (int)w->p_rs_variant;
+    if (v == 4) v = -1;  // LL requested but this message does not qualify
     if (v < 0) {
       int seg;
       size_t off;
@@ -1053,11 +1077,12 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!w || !key) return PCCL_ERR_INVALID_ARGUMENT;
   int64_t *ref = param_ref(w, key);
   const bool is_variant = !strcmp(key, "ag_variant") || !strcmp(key, "rs_variant");
-  if (!ref || value < (is_variant ? -1 : 0)) return PCCL_ERR_INVALID_ARGUMENT;
+  const bool auto_ok = is_variant || !strcmp(key, "ll_max");  // -1 = automatic
+  if (!ref || value < (auto_ok ? -1 : 0)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
-  if ((!strcmp(key, "ag_variant") || !strcmp(key, "rs_variant")) && value > 3) return PCCL_ERR_INVALID_ARGUMENT;
+  if (is_variant && value > 4) return PCCL_ERR_INVALID_ARGUMENT;  // 4 = LL (direct only)
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;

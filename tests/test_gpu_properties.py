@@ -399,3 +399,26 @@ def test_ll_misaligned_buffers_are_bounced():
     want = torch.cat([x[:n].cpu() for x in xs])
     for r in range(p):
         assert torch.equal(ags[r].cpu(), want)
+
+
+def test_param_validation():
+    """Tuning knobs: documented ranges accepted, the rest rejected (include/pccl_b200.h)."""
+    pkg = _pkg()
+    w = pkg.emulated_world(2)
+    cases = [("ll_max", [-1, 0, 8, 1 << 20], [-2]), ("ag_variant", [-1, 0, 1, 2, 3, 4], [-2, 5]),
+             ("rs_variant", [-1, 0, 1, 4], [5]), ("ctas", [0, 1, 320], [-1, 321]), ("nsub", [1, 32], [0, 33]),
+             ("threads", [64, 512], [32, 100, 1024]), ("timeout_ms", [1, 20000], [0]), ("pdl", [0, 1], [-1]),
+             ("local_fence", [0, 1], [-1])]
+    for key, good, bad in cases:
+        old = w.get_param(key)
+        try:
+            for v in good:
+                w.set_param(key, v)
+                assert w.get_param(key) == v
+            for v in bad:
+                with pytest.raises(ValueError):
+                    w.set_param(key, v)
+        finally:
+            w.set_param(key, old)
+    with pytest.raises(ValueError):
+        w.set_param("no_such_knob", 1)
