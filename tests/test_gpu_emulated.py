@@ -245,8 +245,12 @@ def test_empty_payloads():
     for fn in (pkg.ring_all_gather, pkg.recdbl_all_gather, pkg.direct_all_gather):
         outs = pkg.run_ranks(4, lambda c: fn(c, np.zeros(0, np.float32)))
         assert all(o.size == 0 for o in outs)
-    outs = pkg.run_ranks(4, lambda c: pkg.ring_reduce_scatter(c, np.zeros(0, np.float32)))
-    assert all(o.size == 0 for o in outs)
+    for fn in (pkg.ring_reduce_scatter, pkg.rechalf_reduce_scatter, pkg.direct_reduce_scatter):
+        outs = pkg.run_ranks(4, lambda c: fn(c, np.zeros(0, np.float32)))
+        assert all(o.size == 0 for o in outs)
+    # device tensors too (no host round trip)
+    outs = pkg.run_ranks(4, lambda c: pkg.all_gather(c, torch.zeros(0, device="cuda"), algorithm="direct"))
+    assert all(o.numel() == 0 for o in outs)
 
 
 def test_errors():
@@ -267,8 +271,8 @@ def test_errors():
     assert np.array_equal(outs[1], [0, 0, 1, 1])
 
 
-@pytest.mark.parametrize("algo", ["direct", "ring", "recursive"])
-def test_device_side_signature_mismatch_aborts_cleanly(algo):
+@pytest.mark.parametrize("algo,n", [("direct", 4096), ("direct", 1 << 22), ("ring", 4096), ("recursive", 4096)])
+def test_device_side_signature_mismatch_aborts_cleanly(algo, n):
     """A rank whose call signature differs (what a cross-rank size mismatch
     looks like on a real multi-GPU job) must make every rank raise
     LengthMismatch via the device flag protocol — not hang."""
@@ -280,11 +284,13 @@ def test_device_side_signature_mismatch_aborts_cleanly(algo):
     _lib.lib().pccl_emu_debug_meta_skew(w.handle, 2, 0x1234)
     try:
         with pytest.raises(LengthMismatch):
-            pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(4096, device="cuda"), algorithm=algo))
+            pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(n, device="cuda"), algorithm=algo))
+        with pytest.raises(LengthMismatch):  # all-gather too (LL header / READY word)
+            pkg.run_ranks(4, lambda c: pkg.all_gather(c, torch.ones(n // 4, device="cuda"), algorithm=algo))
     finally:
         _lib.lib().pccl_emu_debug_meta_skew(w.handle, 2, 0)
         w.reset_flags()
-    outs = pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(4096, device="cuda"), algorithm=algo))
+    outs = pkg.run_ranks(4, lambda c: pkg.reduce_scatter(c, torch.ones(n, device="cuda"), algorithm=algo))
     assert all(torch.all(o == 4) for o in outs)
 
 
