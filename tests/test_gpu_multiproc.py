@@ -49,3 +49,18 @@ def test_sweep_harness_real_mode(backend, algo, grid, tmp_path):
     recs = S.read_records_csv(csv)
     assert len(recs) == 2 * 4 and all(rec.verified and rec.backend == backend for rec in recs)
     assert out.count("verified") == 2, out[-2000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_real_mode_fuzz(nproc):
+    """Randomised mix of collectives / algorithms / dtypes / sizes / buffer
+    kinds (LL and flag protocols, graphs) checked bit-exact (tests/mp_fuzz.py)."""
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs, box has {_ngpus()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29520 + nproc}", os.path.join(ROOT, "tests", "mp_fuzz.py"),
+           "--iters", "300", "--seed", str(nproc)]
+    r = subprocess.run(cmd, env=dict(os.environ, PCCL_TIMEOUT_MS="10000"), capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count("FUZZ OK") == nproc, out[-4000:]
