@@ -136,15 +136,20 @@ def cpu_reference(p: int, s_bytes: int, dtype: str, algo: str, steps: int, warmu
     for _ in range(p):
         x = rng.standard_normal(n * p).astype(np.float32)
         ins.append(oracle.f32_to_bf16(x) if dtype == "bf16" else x)
-    threads = os.cpu_count() or 1
-    pool = ThreadPoolExecutor(max_workers=min(threads, p))
+    # every host thread this process may use (affinity mask), capped so each
+    # thread still gets >= 16 Ki elements of every chunk
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        threads = os.cpu_count() or 1
+    threads = max(1, min(threads, n // 16384 or 1))
+    pool = ThreadPoolExecutor(max_workers=threads)
     fn = oc.rechalf_reduce_scatter if algo == "recursive" else oc.ring_reduce_scatter
 
     def one_call():
-        # rank-parallel execution: each rank's chunk reduction is independent
-        # once inputs are exchanged; the oracle runs all ranks' steps, so split
-        # the element range across threads (every element's fold order kept).
-        parts = min(threads, 8)
+        # the element range is split across threads (elementwise folds: every
+        # element keeps its reduction order); numpy releases the GIL
+        parts = threads
         bounds = np.linspace(0, n, parts + 1).astype(int)
 
         def run(i):
@@ -163,7 +168,7 @@ def cpu_reference(p: int, s_bytes: int, dtype: str, algo: str, steps: int, warmu
         times.append(time.perf_counter() - t0)
     pool.shutdown()
     t = statistics.mean(times)
-    return t, min(threads, 8)
+    return t, threads
 
 
 # ---------------------------------------------------------------------------
