@@ -311,130 +311,140 @@ def run_gpu(args):
     # ---- extras: the other algorithms / all-gather / NCCL, same bytes ----
     extra = {}
     if not args.no_extra:
-        def measure(fn, k=max(5, args.steps)):
-            for _ in range(3):
-                fn()
-            barrier()
-            t = time_calls(fn, k, stream)
-            world.check()
-            if real:
-                tt = torch.tensor([t], device=dev, dtype=torch.float64)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                t = float(tt.item())
-            return t
-
-        for alg2 in ("direct", "ring", "recursive"):
-            a2 = _lib.ALGOS[alg2]
-            o2 = _lib.ORDERS["recursive" if alg2 == "recursive" else "ring"]
-            world.ensure_staging(int(L.pccl_staging_bytes(1, a2, p, n, code)))
-            if real:
-                f = lambda: _lib.check(L.pccl_reduce_scatter(ghandle, a2, o2, sin.data_ptr(), sout.data_ptr(), n, code,  # noqa: E731
-                                                            stream.cuda_stream))
-            else:
-                f = lambda: _lib.check(L.pccl_emu_reduce_scatter(group.handle, a2, o2, sp, rp, n, code,  # noqa: E731
-                                                                stream.cuda_stream))
-            t = measure(f)
-            extra[f"rs_{args.dtype}_{args.size_mib}MiB_{alg2}"] = {"busbw_gbs": round(busbw(S, p, t), 1),
-                                                                   "us": round(t * 1e6, 1)}
-        # all-gather fp32 64 MiB output (configs[0] / C1 shape)
-        S_ag = 64 << 20
-        n_ag = S_ag // 4 // p
-        if real:
-            ag_in = world.empty(n_ag, torch.float32)
-            ag_out = world.empty(n_ag * p, torch.float32)
-            ag_in.normal_()
-        else:
-            ag_ins = world.empty(n_ag, torch.float32)
-            ag_outs = world.empty(n_ag * p, torch.float32)
-            agsp = _lib.ptr_array([t.data_ptr() for t in ag_ins])
-            agrp = _lib.ptr_array([t.data_ptr() for t in ag_outs])
-        for alg2 in ("direct", "ring", "recursive"):
-            a2 = _lib.ALGOS[alg2]
-            world.ensure_staging(int(L.pccl_staging_bytes(0, a2, p, n_ag, 0)))
-            if real:
-                f = lambda: _lib.check(L.pccl_all_gather(ghandle, a2, ag_in.data_ptr(), ag_out.data_ptr(), n_ag, 0,  # noqa: E731
-                                                        stream.cuda_stream))
-            else:
-                f = lambda: _lib.check(L.pccl_emu_all_gather(group.handle, a2, agsp, agrp, n_ag, 0,  # noqa: E731
-                                                            stream.cuda_stream))
-            t = measure(f)
-            extra[f"ag_f32_64MiB_{alg2}"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
-        if real:
-            nin = torch.empty(n * p, dtype=dtype, device=dev).normal_()
-            nout = torch.empty(n, dtype=dtype, device=dev)
-            t = measure(lambda: dist.reduce_scatter_tensor(nout, nin))
-            extra[f"nccl_rs_{args.dtype}_{args.size_mib}MiB"] = {"busbw_gbs": round(busbw(S, p, t), 1),
-                                                                "us": round(t * 1e6, 1),
-                                                                "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
-            agi = torch.empty(n_ag, dtype=torch.float32, device=dev).normal_()
-            ago = torch.empty(n_ag * p, dtype=torch.float32, device=dev)
-            t = measure(lambda: dist.all_gather_into_tensor(ago, agi))
-            extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
-            del nin, nout, agi, ago
-
-        # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
-        S_h = 256 << 20
-        grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
-        if grids:
-            n_h = S_h // 4 // p
-            if real:
-                h_ag_in, h_ag_out = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
-                h_rs_in, h_rs_out = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
-                h_ag_in.normal_()
-                h_rs_in.normal_()
-            else:
-                hai, hao = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
-                hri, hro = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
-                ptrs = {k: _lib.ptr_array([t.data_ptr() for t in v]) for k, v in
-                        dict(ai=hai, ao=hao, ri=hri, ro=hro).items()}
-            world.ensure_staging(int(L.pccl_staging_bytes(1, 3, p, n_h, 0)))
-            for (N, M) in grids:
-                inter = "recursive" if N >= 4 else "ring"
-                ia = _lib.ALGOS[inter]
+        try:
+            def measure(fn, k=max(5, args.steps)):
+                for _ in range(3):
+                    fn()
+                barrier()
+                t = time_calls(fn, k, stream)
+                world.check()
                 if real:
-                    fa = lambda: _lib.check(L.pccl_hier_all_gather(world.handle, N, M, ia, h_ag_in.data_ptr(),  # noqa: E731
-                                                                  h_ag_out.data_ptr(), n_h, 0, stream.cuda_stream))
-                    fr = lambda: _lib.check(L.pccl_hier_reduce_scatter(world.handle, N, M, ia, h_rs_in.data_ptr(),  # noqa: E731
-                                                                      h_rs_out.data_ptr(), n_h, 0, stream.cuda_stream))
-                else:
-                    fa = lambda: _lib.check(L.pccl_emu_hier_all_gather(world.handle, N, M, ia, ptrs["ai"], ptrs["ao"],  # noqa: E731
-                                                                      n_h, 0, stream.cuda_stream))
-                    fr = lambda: _lib.check(L.pccl_emu_hier_reduce_scatter(world.handle, N, M, ia, ptrs["ri"],  # noqa: E731
-                                                                          ptrs["ro"], n_h, 0, stream.cuda_stream))
-                for nm, f in (("ag", fa), ("rs", fr)):
-                    t = measure(f)
-                    extra[f"hier_{nm}_f32_256MiB_{N}x{M}_{inter}"] = {"busbw_gbs": round(busbw(S_h, p, t), 1),
-                                                                      "us": round(t * 1e6, 1)}
+                    tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    t = float(tt.item())
+                return t
 
-        # C5: FSDP / ZeRO-3 GPT-3-style 7B per-layer shapes (12h^2 + 13h params, h = 4096), bf16
-        if real:
-            P7 = 12 * 4096 * 4096 + 13 * 4096
-            n7 = P7 // p
-            S7 = n7 * p * 2
-            prm = world.empty(n7, torch.bfloat16)
-            full = world.empty(n7 * p, torch.bfloat16)
-            grad = world.empty(n7 * p, torch.bfloat16)
-            gsh = world.empty(n7, torch.bfloat16)
-            prm.normal_()
-            grad.normal_()
-            world.ensure_staging(int(L.pccl_staging_bytes(1, 2, p, n7, 1)))
-            t = measure(lambda: pkg.all_gather_into_tensor(full, prm, comm))
-            extra["fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
-                                             "bytes_out": S7, "algorithm": pkg.choose_algorithm("all_gather", p, S7)}
-            t = measure(lambda: pkg.reduce_scatter_tensor(gsh, grad, comm))
-            extra["fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
-                                             "bytes_in": S7, "algorithm": pkg.choose_algorithm("reduce_scatter", p, S7)}
-            nfull = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev)
-            nprm = torch.empty(n7, dtype=torch.bfloat16, device=dev).normal_()
-            t = measure(lambda: dist.all_gather_into_tensor(nfull, nprm))
-            extra["nccl_fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
-            ngrad = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev).normal_()
-            t = measure(lambda: dist.reduce_scatter_tensor(nprm, ngrad))
-            extra["nccl_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
-            del nfull, nprm, ngrad
+            for alg2 in ("direct", "ring", "recursive"):
+                a2 = _lib.ALGOS[alg2]
+                o2 = _lib.ORDERS["recursive" if alg2 == "recursive" else "ring"]
+                world.ensure_staging(int(L.pccl_staging_bytes(1, a2, p, n, code)))
+                if real:
+                    f = lambda: _lib.check(L.pccl_reduce_scatter(ghandle, a2, o2, sin.data_ptr(), sout.data_ptr(), n, code,  # noqa: E731
+                                                                stream.cuda_stream))
+                else:
+                    f = lambda: _lib.check(L.pccl_emu_reduce_scatter(group.handle, a2, o2, sp, rp, n, code,  # noqa: E731
+                                                                    stream.cuda_stream))
+                t = measure(f)
+                extra[f"rs_{args.dtype}_{args.size_mib}MiB_{alg2}"] = {"busbw_gbs": round(busbw(S, p, t), 1),
+                                                                       "us": round(t * 1e6, 1)}
+            # all-gather fp32 64 MiB output (configs[0] / C1 shape)
+            S_ag = 64 << 20
+            n_ag = S_ag // 4 // p
+            if real:
+                ag_in = world.empty(n_ag, torch.float32)
+                ag_out = world.empty(n_ag * p, torch.float32)
+                ag_in.normal_()
+            else:
+                ag_ins = world.empty(n_ag, torch.float32)
+                ag_outs = world.empty(n_ag * p, torch.float32)
+                agsp = _lib.ptr_array([t.data_ptr() for t in ag_ins])
+                agrp = _lib.ptr_array([t.data_ptr() for t in ag_outs])
+            for alg2 in ("direct", "ring", "recursive"):
+                a2 = _lib.ALGOS[alg2]
+                world.ensure_staging(int(L.pccl_staging_bytes(0, a2, p, n_ag, 0)))
+                if real:
+                    f = lambda: _lib.check(L.pccl_all_gather(ghandle, a2, ag_in.data_ptr(), ag_out.data_ptr(), n_ag, 0,  # noqa: E731
+                                                            stream.cuda_stream))
+                else:
+                    f = lambda: _lib.check(L.pccl_emu_all_gather(group.handle, a2, agsp, agrp, n_ag, 0,  # noqa: E731
+                                                                stream.cuda_stream))
+                t = measure(f)
+                extra[f"ag_f32_64MiB_{alg2}"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
+            if real:
+                nin = torch.empty(n * p, dtype=dtype, device=dev).normal_()
+                nout = torch.empty(n, dtype=dtype, device=dev)
+                t = measure(lambda: dist.reduce_scatter_tensor(nout, nin))
+                extra[f"nccl_rs_{args.dtype}_{args.size_mib}MiB"] = {"busbw_gbs": round(busbw(S, p, t), 1),
+                                                                    "us": round(t * 1e6, 1),
+                                                                    "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
+                agi = torch.empty(n_ag, dtype=torch.float32, device=dev).normal_()
+                ago = torch.empty(n_ag * p, dtype=torch.float32, device=dev)
+                t = measure(lambda: dist.all_gather_into_tensor(ago, agi))
+                extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
+                del nin, nout, agi, ago
+
+            # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
+            S_h = 256 << 20
+            grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
+            if grids:
+                n_h = S_h // 4 // p
+                if real:
+                    h_ag_in, h_ag_out = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
+                    h_rs_in, h_rs_out = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
+                    h_ag_in.normal_()
+                    h_rs_in.normal_()
+                else:
+                    hai, hao = world.empty(n_h, torch.float32), world.empty(n_h * p, torch.float32)
+                    hri, hro = world.empty(n_h * p, torch.float32), world.empty(n_h, torch.float32)
+                    ptrs = {k: _lib.ptr_array([t.data_ptr() for t in v]) for k, v in
+                            dict(ai=hai, ao=hao, ri=hri, ro=hro).items()}
+                world.ensure_staging(int(L.pccl_staging_bytes(1, 3, p, n_h, 0)))
+                for (N, M) in grids:
+                    inter = "recursive" if N >= 4 else "ring"
+                    ia = _lib.ALGOS[inter]
+                    if real:
+                        fa = lambda: _lib.check(L.pccl_hier_all_gather(world.handle, N, M, ia, h_ag_in.data_ptr(),  # noqa: E731
+                                                                      h_ag_out.data_ptr(), n_h, 0, stream.cuda_stream))
+                        fr = lambda: _lib.check(L.pccl_hier_reduce_scatter(world.handle, N, M, ia, h_rs_in.data_ptr(),  # noqa: E731
+                                                                          h_rs_out.data_ptr(), n_h, 0, stream.cuda_stream))
+                    else:
+                        fa = lambda: _lib.check(L.pccl_emu_hier_all_gather(world.handle, N, M, ia, ptrs["ai"], ptrs["ao"],  # noqa: E731
+                                                                          n_h, 0, stream.cuda_stream))
+                        fr = lambda: _lib.check(L.pccl_emu_hier_reduce_scatter(world.handle, N, M, ia, ptrs["ri"],  # noqa: E731
+                                                                              ptrs["ro"], n_h, 0, stream.cuda_stream))
+                    for nm, f in (("ag", fa), ("rs", fr)):
+                        t = measure(f)
+                        extra[f"hier_{nm}_f32_256MiB_{N}x{M}_{inter}"] = {"busbw_gbs": round(busbw(S_h, p, t), 1),
+                                                                          "us": round(t * 1e6, 1)}
+
+            # C5: FSDP / ZeRO-3 GPT-3-style 7B per-layer shapes (12h^2 + 13h params, h = 4096), bf16
+            if real:
+                P7 = 12 * 4096 * 4096 + 13 * 4096
+                n7 = P7 // p
+                S7 = n7 * p * 2
+                prm = world.empty(n7, torch.bfloat16)
+                full = world.empty(n7 * p, torch.bfloat16)
+                grad = world.empty(n7 * p, torch.bfloat16)
+                gsh = world.empty(n7, torch.bfloat16)
+                prm.normal_()
+                grad.normal_()
+                world.ensure_staging(int(L.pccl_staging_bytes(1, 2, p, n7, 1)))
+                t = measure(lambda: pkg.all_gather_into_tensor(full, prm, comm))
+                extra["fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
+                                                 "bytes_out": S7, "algorithm": pkg.choose_algorithm("all_gather", p, S7)}
+                t = measure(lambda: pkg.reduce_scatter_tensor(gsh, grad, comm))
+                extra["fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
+                                                 "bytes_in": S7, "algorithm": pkg.choose_algorithm("reduce_scatter", p, S7)}
+                nfull = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev)
+                nprm = torch.empty(n7, dtype=torch.bfloat16, device=dev).normal_()
+                t = measure(lambda: dist.all_gather_into_tensor(nfull, nprm))
+                extra["nccl_fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
+                ngrad = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev).normal_()
+                t = measure(lambda: dist.reduce_scatter_tensor(nprm, ngrad))
+                extra["nccl_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
+                del nfull, nprm, ngrad
+        except Exception as exc:  # an extra must never cost the headline line
+            extra["error"] = f"{type(exc).__name__}: {exc}"[:300]
+            if rank == 0:
+                print(f"[bench] extra measurements aborted: {exc!r}", file=sys.stderr, flush=True)
 
     # ---- e2e through the public API with host buffers ----
-    e2e = None if args.profile else run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)
+    if args.profile:
+        e2e = None
+    elif "error" in extra:  # a device error poisons the world: no further collectives
+        e2e = {"value": None, "unit": "GB/s", "error": "skipped after: " + extra["error"][:200]}
+    else:
+        e2e = run_e2e(args, pkg, real, p, S, dtype, dev, comm if real else None, dist)
 
     # ---- roofline of the dominant kernel (the measured call itself) ----
     pk, src = peaks()
