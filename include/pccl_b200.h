@@ -108,7 +108,9 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
  * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
  * collectives use the LL protocol — flags inside 16-byte data words, no
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
- * (group size - 1), 0 off). Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
+ * (group size - 1), 0 off), "item_kib" (direct collectives: CTAs claim work
+ * items of this many KiB from a device counter instead of static slices;
+ * default 0 = static; measured: no gain, see DESIGN). Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
 int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
 /* With param "trace" = 1, every launch records per-CTA events (globaltimer ns
@@ -182,6 +184,12 @@ int pccl_probe(pccl_world_t w, int seg_id, int mode, uint32_t dst_mask, size_t b
 int pccl_shuffle(int direction, const void *in, void *out, int N, int M, size_t block_len, int dtype, void *stream);
 /* reduce_inplace (collectives.py:45-52): acc[i] = acc[i] + other[i]. */
 int pccl_reduce_inplace(void *acc, const void *other, size_t count, int dtype, void *stream);
+/* Stream-ordered strided copy between host and device memory (any
+ * direction, cudaMemcpy2DAsync semantics): `height` rows of `width` bytes,
+ * row pitches in bytes. The host-buffer path of the collectives uses it to
+ * move one slice of every chunk / block per call, so host<->device copies of
+ * slice k+1 overlap the collective on slice k (pipelined e2e path). */
+int pccl_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height, void *stream);
 
 /* ---- schedule introspection (host only, no GPU needed) -------------------
  * The step structure the kernels execute, as (step, src_world, dst_world,

@@ -22,6 +22,7 @@ pass ``out=`` a tensor from ``comm.world.empty`` to skip every staging copy.
 from __future__ import annotations
 
 import enum
+import os
 
 import numpy as np
 import torch
@@ -206,6 +207,124 @@ def _upload(comm, args: list, ranks: list, out_bytes: int):
     return sends, recvs
 
 
+# Pipelined host path: host buffers of at least PIPE_MIN_BYTES per rank
+# are moved in slices (one slice of every chunk / block per collective call),
+# so the H2D copy of slice k+1 and the D2H copy of slice k-1 run on the copy
+# engines while the collective of slice k runs. Elementwise the slices
+# compute exactly what the whole call computes (same algorithm, same order).
+PIPE_MIN_BYTES = int(os.environ.get("PCCL_PIPE_MIN_BYTES", 8 << 20))
+PIPE_SLICE_BYTES = int(os.environ.get("PCCL_PIPE_SLICE_BYTES", 8 << 20))
+PIPE_MAX_SLICES = 16
+_PIPE_BUFS = 3
+_side_streams: dict = {}
+
+
+def _pipe_streams(device: torch.device):
+    key = device.index
+    if key not in _side_streams:
+        _side_streams[key] = (torch.cuda.Stream(device), torch.cuda.Stream(device))
+    return _side_streams[key]
+
+
+def _pipeline_slices(row_len: int, es: int, in_bytes: int):
+    """[(offset, length)] in elements over one row (chunk or block), or None
+    when the call is too small to gain from pipelining."""
+    if in_bytes < PIPE_MIN_BYTES or row_len == 0:
+        return None
+    k = max(2, min(PIPE_MAX_SLICES, in_bytes // PIPE_SLICE_BYTES))
+    grain = max(1, 256 // es)  # slices start 256-byte aligned (vector path)
+    cs = -(-row_len // k)
+    cs = -(-cs // grain) * grain
+    out = [(off, min(cs, row_len - off)) for off in range(0, row_len, cs)]
+    return out if len(out) >= 2 else None
+
+
+def _host_pipeline(comm, args: list, ranks: list, reduce: bool, algo: str, order: str, out_numel: int, emu: bool):
+    """Host inputs -> fresh pinned host outputs through the io segment in slices.
+
+    RS: rank r's input is p chunks of L elements; slice (off, ln) uploads
+    column range [off, off+ln) of every chunk (one strided copy) into a
+    contiguous p x ln send buffer, reduce-scatters it (count ln) and downloads
+    the ln results to out[off:off+ln]. AG mirrors it: ln input elements
+    up, a p x ln gathered slice down into column range [off, off+ln) of the
+    p blocks. Buffer reuse is event-ordered: slice k's upload waits for the
+    collective of slice k-3 (pull kernels exit only after every peer finished
+    reading the send buffer), and slice k's collective waits for the download
+    of slice k-3 (its peers may write into the receive buffer as soon as it
+    starts). The decision depends only on sizes, so it is SPMD-uniform (pageable
+inputs are correct too; their uploads are just not asynchronous). Returns
+None when the call is too small to gain."""
+    t0 = args[0].t
+    es = t0.element_size()
+    p = comm.size
+    row_len = t0.numel() // p if reduce else t0.numel()
+    slices = _pipeline_slices(row_len, es, t0.numel() * es)
+    if slices is None:
+        return None
+    cs = slices[0][1]
+    in_sl = (p * cs if reduce else cs) * es
+    out_sl = (cs if reduce else p * cs) * es
+    per_buf = _align(in_sl) + _align(out_sl)
+    io = _ensure_io(comm, _PIPE_BUFS * per_buf)
+    if io is None or io.nbytes < _PIPE_BUFS * per_buf:
+        return None
+    dev = comm.device
+    cur = torch.cuda.current_stream(dev)
+    up, down = _pipe_streams(dev)
+    outs = [torch.empty(out_numel, dtype=t0.dtype, pin_memory=True) for _ in args]
+    bases = {r: io.tensor(r, 0, _PIPE_BUFS * per_buf) for r in ranks}
+    L = lib()
+    ev_comp, ev_down = [], []
+    up.wait_stream(cur)
+    down.wait_stream(cur)
+    for k, (off, ln) in enumerate(slices):
+        b = k % _PIPE_BUFS
+        sends, recvs = [], []
+        for r in ranks:
+            base = bases[r]
+            sends.append(base[b * per_buf: b * per_buf + (p * ln if reduce else ln) * es].view(t0.dtype))
+            ob = b * per_buf + _align(in_sl)
+            recvs.append(base[ob: ob + (ln if reduce else p * ln) * es].view(t0.dtype))
+        with torch.cuda.stream(up):
+            if k >= _PIPE_BUFS:
+                up.wait_event(ev_comp[k - _PIPE_BUFS])
+            for a, snd in zip(args, sends):
+                src = a.t.data_ptr() + off * es
+                if reduce:  # column range of every chunk -> p x ln
+                    st = L.pccl_copy2d(snd.data_ptr(), ln * es, src, row_len * es, ln * es, p, up.cuda_stream)
+                else:
+                    st = L.pccl_copy2d(snd.data_ptr(), ln * es, src, ln * es, ln * es, 1, up.cuda_stream)
+                check(st, "copy2d (upload)")
+            ev_up = torch.cuda.Event()
+            ev_up.record(up)
+        cur.wait_event(ev_up)
+        if k >= _PIPE_BUFS:
+            cur.wait_event(ev_down[k - _PIPE_BUFS])
+        if reduce:
+            _reduce_scatter_device(comm, algo, order, sends, recvs, emu)
+        else:
+            _all_gather_device(comm, algo, sends, recvs, emu)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        ev_comp.append(ev)
+        with torch.cuda.stream(down):
+            down.wait_event(ev)
+            for o, rcv in zip(outs, recvs):
+                dst = o.data_ptr() + off * es
+                if reduce:
+                    st = L.pccl_copy2d(dst, ln * es, rcv.data_ptr(), ln * es, ln * es, 1, down.cuda_stream)
+                else:  # p x ln gathered slice -> column range of every block
+                    st = L.pccl_copy2d(dst, row_len * es, rcv.data_ptr(), ln * es, ln * es, p, down.cuda_stream)
+                check(st, "copy2d (download)")
+            evd = torch.cuda.Event()
+            evd.record(down)
+            ev_down.append(evd)
+    cur.wait_stream(down)
+    cur.wait_stream(up)
+    cur.synchronize()
+    return outs
+
+
 _REDUCE_DTYPES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 
 
@@ -288,6 +407,11 @@ def _run(comm, buf, reduce: bool, algo: str, order: str, out=None):
         sizes = [a.t.numel() for a in args]
         if len(set(sizes)) > 1 or len({a.t.dtype for a in args}) > 1:
             raise LengthMismatch(f"buffer sizes/dtypes differ across ranks: {sizes}")
+        if all(a.host for a in args):
+            piped = _host_pipeline(comm, args, ranks, reduce, algo, order, out_numel, emu)
+            if piped is not None:
+                comm.world.check()
+                return [_finish(a, h) for a, h in zip(args, piped)]
         if all(a.host for a in args):
             es = args[0].t.element_size()
             sends, recvs = _upload(comm, args, ranks, out_numel * es)

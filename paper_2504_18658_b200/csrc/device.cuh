@@ -32,7 +32,8 @@
 #define PCCL_MAX_CTAS 320
 #define PCCL_NSLOTS 256
 #define PCCL_CTRL_OFF (3 * PCCL_MAXR * PCCL_MAX_CTAS)
-#define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter
+#define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter,
+                                              //   [2] work-item counter (direct kernels, see for_items)
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
 // After the slots: world-level control words, then the LL (low-latency)
 // message regions (see "LL protocol" below). Both live in segment 0, so every
@@ -69,6 +70,7 @@ struct LaunchParams {
   int tma_stages;   // TMA ring depth
   uint32_t tma_tile;  // TMA tile bytes
   int local_fence;  // 1: pull-kernel signals fence at gpu scope (data is in the writer's own HBM)
+  int64_t item;     // direct kernels: units per dynamically claimed work item (0: static CTA slices)
   int64_t timeout_ns;
   int64_t blk;              // units per sub-block
   int64_t sub_stride;       // stride between sub-blocks (shared layout)
@@ -177,6 +179,7 @@ struct CtaEpilogue {
       const unsigned long long old = atomicAdd(ctrl + 1, 1ull);
       if (old == (unsigned long long)(c.P->ctas - 1)) {
         ctrl[1] = 0;
+        ctrl[2] = 0;  // work-item counter (every CTA's last claim returned before it got here)
         *reinterpret_cast<volatile unsigned long long *>(ctrl) = c.epoch;
         if (c.ll_peers) {
           volatile uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
@@ -490,6 +493,33 @@ __device__ __forceinline__ void cta_subslice(const Ctx &c, int t, int64_t &lo, i
   split32(e - a, c.P->nsub, t, sa, se);
   lo = a + sa;
   hi = a + se;
+}
+
+// Dynamic work distribution for the single-step (direct) kernels. Measured
+// with tools/trace.py at p=4, 128 MiB: with static CTA slices the CTAs'
+// finishing times spread over ~40 us (push AG: 108..149 us) because NVLink
+// arbitration is not fair between SMs, and the link idles in the tail.
+// Instead every CTA claims items from a per-row counter in its own slot
+// (CTRL[2], local atomics; the row's last CTA resets it in CtaEpilogue), and
+// prefetches its next claim while moving the current item. The flag protocol
+// is unchanged: CTA b still signals / waits on the peers' CTA b, and since a
+// rank's kernel completes only after all of its CTAs' waits, the union over
+// b still covers every item of every peer.
+template <typename F>
+__device__ __forceinline__ void for_items(const Ctx &c, int64_t total, F &&body) {
+  __shared__ long long s_item[2];
+  unsigned long long *ctr = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF + 2);
+  if (threadIdx.x == 0) s_item[0] = (long long)atomicAdd(ctr, 1ull);
+  __syncthreads();
+  long long cur = s_item[0];
+  for (int k = 1; cur < total; ++k) {
+    unsigned long long nx = 0;
+    if (threadIdx.x == 0) nx = atomicAdd(ctr, 1ull);  // in flight while this item moves
+    body((int64_t)cur);
+    if (threadIdx.x == 0) s_item[k & 1] = (long long)nx;
+    __syncthreads();
+    cur = s_item[k & 1];
+  }
 }
 
 // --------------------------------------------------------------------------

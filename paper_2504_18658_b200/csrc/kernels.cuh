@@ -58,11 +58,26 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);
   if (!cta_wait_mask(c, peers, 0, true)) return;
-  for (int i = 1; i < c.gs; ++i) {
-    const int q = (c.gi + i) % c.gs;  // rotate so every rank reads a different peer
-    const char *src = P.send[c.world(q)];
-    for (int t = 0; t < P.nsubblk; ++t)
-      copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t), src + (int64_t)t * P.send_sub_stride * U, lo, hi);
+  if (P.item > 0) {
+    // items (range j, sub-block t, source i), source fastest so that the
+    // CTAs in flight spread over all peers
+    const int nd = c.gs - 1;
+    const int64_t nj = (P.blk + P.item - 1) / P.item;
+    for_items(c, nj * nd * P.nsubblk, [&](int64_t id) {
+      const int64_t j = id / (nd * P.nsubblk);
+      const int rem = (int)(id - j * nd * P.nsubblk);
+      const int q = (c.gi + 1 + rem % nd) % c.gs, t = rem / nd;
+      const int64_t a = j * P.item, e = min(a + P.item, P.blk);
+      copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t),
+                             P.send[c.world(q)] + (int64_t)t * P.send_sub_stride * U, a, e);
+    });
+  } else {
+    for (int i = 1; i < c.gs; ++i) {
+      const int q = (c.gi + i) % c.gs;  // rotate so every rank reads a different peer
+      const char *src = P.send[c.world(q)];
+      for (int t = 0; t < P.nsubblk; ++t)
+        copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t), src + (int64_t)t * P.send_sub_stride * U, lo, hi);
+    }
   }
   cta_exit(c, peers, peers);
 }
@@ -165,13 +180,27 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (!cta_wait_mask(c, peers, 0, true)) return;
-  for (int i = 1; i < c.gs; ++i) {
-    const int q = (c.gi + i) % c.gs;
-    char *dst = P.recv[c.world(q)];
-    for (int t = 0; t < P.nsubblk; ++t)
-      store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
+  if (P.item > 0) {
+    // items (range j, sub-block t, destination i), destination fastest
+    const int nd = c.gs - 1;
+    const int64_t nj = (P.blk + P.item - 1) / P.item;
+    for_items(c, nj * nd * P.nsubblk, [&](int64_t id) {
+      const int64_t j = id / (nd * P.nsubblk);
+      const int rem = (int)(id - j * nd * P.nsubblk);
+      const int q = (c.gi + 1 + rem % nd) % c.gs, t = rem / nd;
+      const int64_t a = j * P.item, e = min(a + P.item, P.blk);
+      store_units<U>(ag_block<U>(P, P.recv[c.world(q)], c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U,
+                     a, e);
+    });
+  } else {
+    for (int i = 1; i < c.gs; ++i) {
+      const int q = (c.gi + i) % c.gs;
+      char *dst = P.recv[c.world(q)];
+      for (int t = 0; t < P.nsubblk; ++t)
+        store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
+    }
   }
-  cta_signal_mask(c, peers, 1);  // my block has landed in your recv
+  cta_signal_mask(c, peers, 1);  // my block (this CTA's items of it) has landed in your recv
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
   if (!cta_wait_mask(c, peers, 1, false)) return;
 }
@@ -553,10 +582,22 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   split32(P.blk, P.ctas, c.b, lo, hi);
   const T *own = reinterpret_cast<const T *>(P.send[c.r]);
   if (PUSH) {
-    for (int i = 1; i < gs; ++i) {
-      const int q = (gi + i) % gs;
-      T *dst = reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk;
-      copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
+    if (P.item > 0) {  // items (range j, destination i), destination fastest
+      const int nd = gs - 1;
+      const int64_t nj = (P.blk + P.item - 1) / P.item;
+      for_items(c, nj * nd, [&](int64_t id) {
+        const int64_t j = id / nd;
+        const int q = (gi + 1 + (int)(id - j * nd)) % gs;
+        const int64_t a = j * P.item, e = min(a + P.item, P.blk);
+        copy_typed<T>(reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk,
+                      own + P.base[c.y] + (int64_t)q * P.istride, a, e);
+      });
+    } else {
+      for (int i = 1; i < gs; ++i) {
+        const int q = (gi + i) % gs;
+        T *dst = reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk;
+        copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
+      }
     }
     cta_signal_mask(c, peers, 1);  // my chunks have landed
     if (!cta_wait_mask(c, peers, 1, false)) return;
@@ -576,7 +617,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
       src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]) + P.base[c.y] + (int64_t)gi * P.istride;
   }
   const int nt = blockDim.x;
-  for (int j = 0; j < P.nsubblk; ++j) {
+  auto fold = [&](int j, int64_t lo, int64_t hi) {
     const int64_t off = (int64_t)j * P.sub_stride;
     T *dst = reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
     for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
@@ -610,6 +651,16 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
       }
       dst[e] = R::store(acc);
     }
+  };
+  if (!PUSH && P.item > 0) {  // pull: items (range, sub-block)
+    const int64_t nj = (P.blk + P.item - 1) / P.item;
+    for_items(c, nj * P.nsubblk, [&](int64_t id) {
+      const int64_t j = id / P.nsubblk;
+      const int64_t a = j * P.item;
+      fold((int)(id - j * P.nsubblk), a, min(a + P.item, P.blk));
+    });
+  } else {
+    for (int j = 0; j < P.nsubblk; ++j) fold(j, lo, hi);
   }
   if (!PUSH) cta_exit(c, peers, peers);
 }

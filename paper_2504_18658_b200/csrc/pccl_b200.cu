@@ -62,6 +62,7 @@ struct pccl_world {
   int poisoned = 0;  // sticky device error
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
+  int64_t p_item_kib = 0;  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
@@ -350,6 +351,12 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   const int64_t epu = U / (int64_t)es > 0 ? U / (int64_t)es : 1;  // elements per unit
   auto units = [&](int64_t e) { return (pl.coll == PCCL_ALL_GATHER) ? e * (int64_t)es / U : e / epu; };
   P.blk = units(pl.blk);
+  if (pl.algo == A_DIRECT && pl.variant != 4 && w->p_item_kib > 0) {
+    // work-item size in units, a multiple of 32 units (the static slicing grain)
+    int64_t it = (w->p_item_kib * 1024 / U) / 32 * 32;
+    if (pl.coll != PCCL_ALL_GATHER) it = (w->p_item_kib * 1024 / (int64_t)es / epu) / 32 * 32;
+    P.item = std::max<int64_t>(32, it);
+  }
   P.sub_stride = units(pl.sub_stride);
   P.istride = units(pl.istride);
   P.send_sub_stride = units(pl.send_sub_stride);
@@ -974,6 +981,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
   if (const char *t = getenv("PCCL_LOCAL_FENCE")) w->p_local_fence = atoi(t);
   if (const char *t = getenv("PCCL_LL_MAX")) w->p_ll_max = atoll(t);
+  if (const char *t = getenv("PCCL_ITEM_KIB")) w->p_item_kib = atoll(t);
   if (const char *t = getenv("PCCL_PDL")) w->p_pdl = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);
   if (const char *t = getenv("PCCL_RS_VARIANT")) w->p_rs_variant = atoi(t);
@@ -1070,6 +1078,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
+  if (!strcmp(key, "item_kib")) return &w->p_item_kib;
   return nullptr;
 }
 
@@ -1382,6 +1391,16 @@ int pccl_shuffle(int direction, const void *in, void *out, int N, int M, size_t 
     default: k_shuffle<1><<<grid, kThreads, 0, s>>>((const char *)in, (char *)out, A, Bd, blk); break;
   }
   CK(cudaGetLastError());
+  return PCCL_SUCCESS;
+}
+
+int pccl_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height, void *stream) {
+  if (width == 0 || height == 0) return PCCL_SUCCESS;
+  if (!dst || !src || dpitch < width || spitch < width) return PCCL_ERR_INVALID_ARGUMENT;
+  if (cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess) {
+    cudaGetLastError();
+    return PCCL_ERR_CUDA;
+  }
   return PCCL_SUCCESS;
 }
 

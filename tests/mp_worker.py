@@ -69,6 +69,31 @@ def main() -> int:
             check(f"rs_direct_rec_n{n}", pkg.direct_reduce_scatter(comm, rs_in[rank], order="recursive"), want)
 
     sync_point("flat")
+    # pipelined host path (slices of every chunk / block, copies overlapped
+    # with the collectives): small slice size so several slices run
+    from paper_2504_18658_b200 import collectives as C
+
+    saved = (C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES)
+    C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES = 256 << 10, 64 << 10
+    try:
+        n = 200_003
+        rs_in = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+        ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+        pinned = torch.from_numpy(rs_in[rank]).pin_memory()
+        check("pipe_rs_ring", pkg.ring_reduce_scatter(comm, rs_in[rank]), oracle.ring_reduce_scatter(rs_in)[rank])
+        check("pipe_rs_direct_pinned", pkg.direct_reduce_scatter(comm, pinned).numpy(),
+              oracle.ring_reduce_scatter(rs_in)[rank])
+        if pow2:
+            check("pipe_rs_rechalf", pkg.rechalf_reduce_scatter(comm, pinned).numpy(),
+                  oracle.rechalf_reduce_scatter(rs_in)[rank])
+        want_ag = oracle.ring_all_gather(ag_in)[rank]
+        check("pipe_ag_ring", pkg.ring_all_gather(comm, ag_in[rank]), want_ag)
+        check("pipe_ag_direct_pinned", pkg.direct_all_gather(comm, torch.from_numpy(ag_in[rank]).pin_memory()).numpy(),
+              want_ag)
+    finally:
+        C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES = saved
+
+    sync_point("pipelined_host")
     # bf16 on device tensors, both through staging and through symmetric buffers
     n = 65536 + 8
     ins = [oracle.f32_to_bf16(rng.standard_normal(n * p).astype(np.float32)) for _ in range(p)]

@@ -209,6 +209,111 @@ def test_large_fp32_normal_bit_exact_vs_oracle(p):
             assert _bits_equal(outs[r], want[r]), (algo, r)
 
 
+@pytest.fixture
+def small_pipeline(monkeypatch):
+    """Pipelined host path with small slices (several slices per call), and
+    a spy that records how many slices each pipelined call used."""
+    from paper_2504_18658_b200 import collectives as C
+
+    monkeypatch.setattr(C, "PIPE_MIN_BYTES", 256 << 10)
+    monkeypatch.setattr(C, "PIPE_SLICE_BYTES", 64 << 10)
+    used = []
+    real = C._pipeline_slices
+
+    def spy(*a):
+        sl = real(*a)
+        used.append(0 if sl is None else len(sl))
+        return sl
+
+    monkeypatch.setattr(C, "_pipeline_slices", spy)
+    return used
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("algo", ["ring", "recursive", "direct"])
+def test_host_pipeline_reduce_scatter_bit_exact(p, algo, small_pipeline):
+    """Host inputs large enough to be sliced: numpy (pageable) and pinned
+    tensors give the same bits as the oracle of the named algorithm."""
+    pkg = _pkg()
+    n = 50_003  # ragged: the last slice is short and unaligned
+    rng = np.random.default_rng(p)
+    ins = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    fn = {"ring": pkg.ring_reduce_scatter, "recursive": pkg.rechalf_reduce_scatter,
+          "direct": pkg.direct_reduce_scatter}[algo]
+    want = (oracle.rechalf_reduce_scatter if algo == "recursive" else oracle.ring_reduce_scatter)(ins)
+    outs = pkg.run_ranks(p, lambda c: fn(c, ins[c.rank]))
+    pins = [torch.from_numpy(x).pin_memory() for x in ins]
+    outs_pinned = pkg.run_ranks(p, lambda c: fn(c, pins[c.rank]))
+    assert small_pipeline and min(small_pipeline) >= 3, small_pipeline
+    for r in range(p):
+        assert _bits_equal(outs[r], want[r]), r
+        assert outs_pinned[r].is_pinned() and _bits_equal(outs_pinned[r].numpy(), want[r]), r
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_host_pipeline_bf16_matches_device_path(p, small_pipeline):
+    pkg = _pkg()
+    n = 70_001
+    g = torch.Generator().manual_seed(p)
+    ins = [torch.randn(n * p, generator=g).to(torch.bfloat16) for _ in range(p)]
+    host = pkg.run_ranks(p, lambda c: pkg.rechalf_reduce_scatter(c, ins[c.rank].pin_memory()))
+    dev = pkg.run_ranks(p, lambda c: pkg.rechalf_reduce_scatter(c, ins[c.rank].cuda()))
+    assert small_pipeline and max(small_pipeline) >= 3
+    for r in range(p):
+        assert torch.equal(host[r].view(torch.int16), dev[r].cpu().view(torch.int16)), r
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("dtype", [np.float32, np.int32, np.uint8])
+def test_host_pipeline_all_gather_byte_exact(p, dtype, small_pipeline):
+    pkg = _pkg()
+    n = 300_007 if dtype == np.uint8 else 200_011
+    rng = np.random.default_rng(7)
+    ins = [rng.integers(0, 255, n).astype(dtype) for _ in range(p)]
+    fns = [pkg.ring_all_gather, pkg.direct_all_gather] + ([pkg.recdbl_all_gather] if p & (p - 1) == 0 else [])
+    for fn in fns:
+        outs = pkg.run_ranks(p, lambda c: fn(c, torch.from_numpy(ins[c.rank]).pin_memory()))
+        want = np.concatenate(ins)
+        for r in range(p):
+            assert np.array_equal(outs[r].numpy(), want), (fn.__name__, r)
+    assert small_pipeline and min(small_pipeline) >= 3
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("item_kib", [16, 64])
+def test_direct_dynamic_work_items_bit_exact(p, item_kib):
+    """Direct kernels with dynamically claimed work items (param item_kib):
+    AG pull / push and RS pull / push give the oracle's bits."""
+    pkg = _pkg()
+    n = 300_001
+    rng = np.random.default_rng(p + item_kib)
+    ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+    rs_in = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    want_ag = np.concatenate(ag_in)
+    want_rs = oracle.ring_reduce_scatter(rs_in)
+
+    def body(c):
+        w = c.world
+        w.set_param("item_kib", item_kib)
+        res = []
+        try:
+            for v in (0, 1):
+                w.set_param("ag_variant", v)
+                w.set_param("rs_variant", v)
+                res.append(pkg.direct_all_gather(c, torch.from_numpy(ag_in[c.rank]).cuda()).cpu().numpy())
+                res.append(pkg.direct_reduce_scatter(c, torch.from_numpy(rs_in[c.rank]).cuda()).cpu().numpy())
+        finally:
+            w.set_param("item_kib", 0)
+            w.set_param("ag_variant", -1)
+            w.set_param("rs_variant", -1)
+        return res
+
+    outs = pkg.run_ranks(p, body)
+    for r in range(p):
+        for i, got in enumerate(outs[r]):
+            assert _bits_equal(got, want_ag if i % 2 == 0 else want_rs[r]), (r, i)
+
+
 def test_back_to_back_calls_reuse_buffers():
     """Epoch flags never reset: many consecutive calls stay correct."""
     pkg = _pkg()

@@ -14,6 +14,7 @@ def main():
     ap.add_argument("--variant", type=int, default=-1); ap.add_argument("--size-mib", type=int, default=128)
     ap.add_argument("--size-kib", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0); ap.add_argument("--nsub", type=int, default=1)
+    ap.add_argument("--item-kib", type=int, default=-1)
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"])); torch.cuda.set_device(dev)
@@ -29,6 +30,7 @@ def main():
     w.set_param("ag_variant" if kind == "ag" else "rs_variant", a.variant)
     if a.ctas: w.set_param("ctas", a.ctas)
     w.set_param("nsub", a.nsub)
+    if a.item_kib >= 0: w.set_param("item_kib", a.item_kib)
     st = torch.cuda.current_stream(dev).cuda_stream
     def f():
         if kind == "ag": _lib.check(L.pccl_all_gather(comm.handle, alg, sin.data_ptr(), sout.data_ptr(), n, code, st))
@@ -57,7 +59,7 @@ def main():
     outs = [None] * p
     dist.all_gather_object(outs, "\n".join(out))
     if rank == 0:
-        print(f"== {a.coll} {a.algo} variant={a.variant} p={p} {S >> 10} KiB ctas={a.ctas or 'auto'} nsub={a.nsub}")
+        print(f"== {a.coll} {a.algo} variant={a.variant} p={p} {S >> 10} KiB ctas={a.ctas or 'auto'} nsub={a.nsub} item_kib={a.item_kib}")
         for o in outs[:2]: print(o)
     dist.barrier(); dist.destroy_process_group()
 

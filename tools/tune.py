@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--variants", default="-1")
     ap.add_argument("--tma", default="4x32768", help="stages x tile bytes list, comma separated")
+    ap.add_argument("--items", default="64", help="item_kib list (direct kernels; 0 = static CTA slices)")
     args = ap.parse_args()
     rank = int(os.environ["RANK"])
     p = int(os.environ["WORLD_SIZE"])
@@ -72,8 +73,11 @@ def main():
                   world.set_param("tma_tile", tile)
               for thr, ctas in [(th, ct) for th in map(int, args.threads.split(",")) for ct in map(int, args.ctas.split(","))]:
                 world.set_param("threads", thr)
-                for nsub in map(int, args.nsub.split(",")):
+                for nsub, item in [(ns, it) for ns in map(int, args.nsub.split(",")) for it in map(int, args.items.split(","))]:
+                    if item != int(args.items.split(",")[0]) and algo != "direct":
+                        continue
                     world.set_tuning(ctas, nsub)
+                    world.set_param("item_kib", item)
                     if kind == "ag":
                         f = lambda: _lib.check(L.pccl_all_gather(comm.handle, a, sin.data_ptr(), sout.data_ptr(), n,  # noqa
                                                                 code, stream.cuda_stream))
@@ -98,10 +102,10 @@ def main():
                     us = float(t) * 1e3
                     bw = S * (p - 1) / p / (us * 1e-6) / 1e9
                     results.append(dict(coll=coll, algo=algo, variant=variant, stages=stg, tile=tile, ctas=ctas, threads=thr,
-                                        nsub=nsub, us=round(us, 1), busbw=round(bw, 1)))
+                                        nsub=nsub, item_kib=item, us=round(us, 1), busbw=round(bw, 1)))
                     if rank == 0:
                         print(f"p={p} {coll:8s} {algo:9s} v={variant} tma={stg}x{tile:6d} thr={thr:3d} ctas={ctas:4d} nsub={nsub:2d} "
-                              f"{us:9.1f} us {bw:7.1f} GB/s", flush=True)
+                              f"item={item:3d} {us:9.1f} us {bw:7.1f} GB/s", flush=True)
               world.set_param("ag_variant", -1)
               world.set_param("rs_variant", -1)
     # NCCL reference points
