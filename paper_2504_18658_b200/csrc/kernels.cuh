@@ -620,10 +620,22 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   auto fold = [&](int j, int64_t lo, int64_t hi) {
     const int64_t off = (int64_t)j * P.sub_stride;
     T *dst = reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += nt) {
-      T raw[MAXP];
+    // EU elements per thread per iteration keep >= 8 independent 16-byte
+    // loads in flight also for small groups (p = 2: 2 leaves per element)
+    constexpr int EU = MAXP >= 8 ? 1 : 8 / MAXP;
+    for (int64_t e0 = lo + threadIdx.x; e0 < hi; e0 += (int64_t)EU * nt) {
+      T rawu[EU][MAXP];
 #pragma unroll
-      for (int i = 0; i < MAXP; ++i) raw[i] = (i < gs) ? ld_peer(src[i] + off + e) : T{};
+      for (int u = 0; u < EU; ++u) {
+        const int64_t e = e0 + (int64_t)u * nt;
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i) rawu[u][i] = (i < gs && e < hi) ? ld_peer(src[i] + off + e) : T{};
+      }
+#pragma unroll
+      for (int u = 0; u < EU; ++u) {
+      const int64_t e = e0 + (int64_t)u * nt;
+      if (e >= hi) break;
+      const T *raw = rawu[u];
       Acc acc;
       if (ORDER == O_REC) {
         Acc v[MAXP];
@@ -650,6 +662,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
           if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
       }
       dst[e] = R::store(acc);
+      }
     }
   };
   if (!PUSH && P.item > 0) {  // pull: items (range, sub-block)

@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--variants", default="-1")
     ap.add_argument("--tma", default="4x32768", help="stages x tile bytes list, comma separated")
-    ap.add_argument("--items", default="64", help="item_kib list (direct kernels; 0 = static CTA slices)")
+    ap.add_argument("--items", default="0", help="item_kib list (direct kernels; 0 = static CTA slices)")
     args = ap.parse_args()
     rank = int(os.environ["RANK"])
     p = int(os.environ["WORLD_SIZE"])
