@@ -486,6 +486,11 @@ def run_gpu(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(t_call * 1e3, 5),
+            # busbw is a per-GPU figure by definition (the metric's "... vs 900 GB/s" per GPU);
+            # the whole job moves value x ranks bus bytes per second
+            "value_is": "per-GPU bus bandwidth busbw = (S/t)(p-1)/p, t = max over ranks; whole-job bus "
+                        "bytes/s in aggregate_gbs",
+            "aggregate_gbs": round(value * p, 1),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,

@@ -862,6 +862,33 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant
   ll_finish(c, s_tag, code);
 }
 
+// TMA variant of the probe (modes 4 push / 5 pull): one thread per CTA moves
+// its range through a shared-memory ring with cp.async.bulk (bulk loads from
+// the source, bulk stores to the destination), the data path of the TMA
+// collective variants.
+__global__ void __launch_bounds__(kThreads) k_probe_tma(char *local, const LaunchParams P, uint32_t dst_mask,
+                                                        int64_t units, int mode) {
+  extern __shared__ __align__(128) char dsm[];
+  int peers[PCCL_MAXR], np = 0;
+  for (int q = 0; q < PCCL_MAXR; ++q)
+    if ((dst_mask >> q) & 1u) peers[np++] = q;
+  if (np == 0) return;
+  const int q = peers[blockIdx.x % np];
+  const int per_peer_ctas = (gridDim.x + np - 1 - (blockIdx.x % np)) / np;
+  int64_t lo, hi;
+  split32(units, per_peer_ctas, blockIdx.x / np, lo, hi);
+  TmaRing R = tma_ring_setup(dsm, P.tma_stages, P.tma_tile);
+  if (threadIdx.x == 0) {
+    char *rem = P.recv[q] + lo * 16, *loc = local + lo * 16;
+    tma_copy_segments(R, 1, [&](int, char *&d, const char *&s, int64_t &len) {
+      len = (hi - lo) * 16;
+      d = mode == 4 ? rem : loc;
+      s = mode == 4 ? loc : rem;
+    });
+  }
+  __syncthreads();
+}
+
 // ============================================================================
 // raw NVLink probe (debug): every CTA streams 16-byte vectors to (push) or
 // from (pull) the peers in dst_mask, round-robin by CTA; no flags, no order.

@@ -1359,7 +1359,15 @@ int pccl_probe(pccl_world_t w, int seg_id, int mode, uint32_t dst_mask, size_t b
   for (int q = 0; q < w->nranks; ++q) P.recv[q] = S.ptr[q] ? S.ptr[q] + S.bytes / 2 : nullptr;
   dst_mask &= ~(1u << w->rank);
   CK(cudaSetDevice(w->device));
-  k_probe<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(S.ptr[w->rank], P, dst_mask, (int64_t)(bytes / 16), mode);
+  if (mode == 4 || mode == 5) {
+    P.tma_stages = (int)w->p_tma_stages;
+    P.tma_tile = (uint32_t)w->p_tma_tile;
+    const size_t smem = (size_t)P.tma_stages * P.tma_tile + 8 * (size_t)P.tma_stages;
+    CK(cudaFuncSetAttribute((const void *)k_probe_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_probe_tma<<<ctas, kThreads, smem, (cudaStream_t)stream>>>(S.ptr[w->rank], P, dst_mask, (int64_t)(bytes / 16), mode);
+  } else {
+    k_probe<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(S.ptr[w->rank], P, dst_mask, (int64_t)(bytes / 16), mode);
+  }
   CK(cudaGetLastError());
   return PCCL_SUCCESS;
 }

@@ -12,7 +12,8 @@ def main():
     import argparse
     ap = argparse.ArgumentParser()
     ap.add_argument("--pats", default="uni,bi,a2a,ring,one2all")
-    ap.add_argument("--modes", default="0,1", help="0 push16 1 pull16 2 push32 3 pull32 (bytes per access)")
+    ap.add_argument("--modes", default="0,1", help="0 push16 1 pull16 2 push32 3 pull32 (bytes per access); "
+                    "4 / 5 = TMA bulk push / pull (PROBE_TMA=stages x tile); 9 = copy-engine push (cudaMemcpyAsync into each peer, one stream per peer)")
     ap.add_argument("--ctas", default="8,16,32,64,128")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -28,7 +29,13 @@ def main():
     pats = {"uni": lambda r: (1 << 1) if r == 0 else 0, "bi": lambda r: (1 << (1 - r)) if r < 2 else 0,
             "a2a": lambda r: ((1 << p) - 1) & ~(1 << r), "ring": lambda r: 1 << ((r + 1) % p),
             "one2all": lambda r: (((1 << p) - 1) & ~1) if r == 0 else 0}
-    names = {0: "push16", 1: "pull16", 2: "push32", 3: "pull32"}
+    names = {0: "push16", 1: "pull16", 2: "push32", 3: "pull32", 4: "tma_push", 5: "tma_pull", 9: "ce_push"}
+    ap2 = os.environ.get("PROBE_TMA", "")  # "stages x tile", e.g. 4x32768
+    if ap2:
+        stg, tile = map(int, ap2.split("x"))
+        w.set_param("tma_stages", stg)
+        w.set_param("tma_tile", tile)
+    peer_streams = [torch.cuda.Stream(dev) for _ in range(p)]
     for pat in a.pats.split(","):
         fm = pats[pat]
         for mode in map(int, a.modes.split(",")):
@@ -37,7 +44,18 @@ def main():
                 npeers = bin(mask).count("1")
                 per = (B // max(1, npeers)) // 32 * 32
                 def f():
-                    if mask:
+                    if mask and mode == 9:
+                        src = seg.ptr(rank)
+                        for q in range(p):
+                            if (mask >> q) & 1:
+                                ps = peer_streams[q]
+                                ps.wait_stream(st)
+                                _lib.check(L.pccl_copy2d(seg.ptr(q) + B + (rank if rank < q else rank - 1) * per, per, src, per, per, 1,
+                                                         ps.cuda_stream))
+                        for q in range(p):
+                            if (mask >> q) & 1:
+                                st.wait_stream(peer_streams[q])
+                    elif mask:
                         _lib.check(L.pccl_probe(w.handle, seg.id, mode, mask, per, ctas, st.cuda_stream))
                 for _ in range(3): f()
                 torch.cuda.synchronize(); dist.barrier()
