@@ -104,7 +104,8 @@ int pccl_world_set_tuning(pccl_world_t w, int ctas, int nsub, int threads);
 int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
 /* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "threads" (per
  * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
- * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL), "tma_stages",
+ * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL, 5 copy engine (AG ring /
+ * recursive doubling, see pccl_ce_available)), "tma_stages",
  * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
  * collectives use the LL protocol — flags inside 16-byte data words, no
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
@@ -189,6 +190,11 @@ int pccl_reduce_inplace(void *acc, const void *other, size_t count, int dtype, v
  * row pitches in bytes. The host-buffer path of the collectives uses it to
  * move one slice of every chunk / block per call, so host<->device copies of
  * slice k+1 overlap the collective on slice k (pipelined e2e path). */
+/* 1 when the copy-engine all-gather (param ag_variant = 5) can run on this
+ * device: stream memory operations (64-bit) are available. The variant takes
+ * ring / recursive doubling into a registered (symmetric) output outside
+ * stream capture, in real mode; any other call falls back to the kernels. */
+int pccl_ce_available(int device);
 int pccl_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height, void *stream);
 
 /* ---- schedule introspection (host only, no GPU needed) -------------------

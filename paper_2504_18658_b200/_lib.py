@@ -65,6 +65,7 @@ _SIGS = {
     "pccl_shuffle": (_i, [_i, _vp, _vp, _i, _i, _sz, _i, _vp]),
     "pccl_reduce_inplace": (_i, [_vp, _vp, _sz, _i, _vp]),
     "pccl_copy2d": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _vp]),
+    "pccl_ce_available": (_i, [_i]),
     "pccl_schedule": (_i, [_i, _i, _i, _i, _i, _sz, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(_i)]),
 }
 

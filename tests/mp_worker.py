@@ -69,6 +69,32 @@ def main() -> int:
             check(f"rs_direct_rec_n{n}", pkg.direct_reduce_scatter(comm, rs_in[rank], order="recursive"), want)
 
     sync_point("flat")
+    # copy-engine all-gather (ag_variant 5): symmetric outputs, mixed with
+    # kernel calls on the same group (separate counters must not interfere)
+    from paper_2504_18658_b200 import _lib as _L
+
+    if _L.lib().pccl_ce_available(torch.cuda.current_device()):
+        w = comm.world
+        for n in (1, 37, 4096, 300_000, 1 << 21):
+            ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+            want = oracle.ring_all_gather(ag_in)[rank]
+            x = torch.from_numpy(ag_in[rank]).cuda()
+            out = w.empty(n * p, torch.float32)
+            for it in range(3):
+                for algo in (["ring", "recursive"] if pow2 else ["ring"]):
+                    for variant in (5, -1):
+                        w.set_param("ag_variant", variant)
+                        out.fill_(float("nan"))
+                        pkg.all_gather_into_tensor(out, x, comm, algorithm=algo)
+                        check(f"ce_ag_{algo}_v{variant}_n{n}_{it}", out.cpu().numpy(), want)
+            # in place: my block already sits in the output
+            w.set_param("ag_variant", 5)
+            out.zero_()
+            out[rank * n:(rank + 1) * n].copy_(x)
+            pkg.all_gather_into_tensor(out, out[rank * n:(rank + 1) * n], comm, algorithm="ring")
+            check(f"ce_ag_inplace_n{n}", out.cpu().numpy(), want)
+        w.set_param("ag_variant", -1)
+    sync_point("copy_engine")
     # pipelined host path (slices of every chunk / block, copies overlapped
     # with the collectives): small slice size so several slices run
     from paper_2504_18658_b200 import collectives as C

@@ -60,9 +60,11 @@ def main():
             world.ensure_staging(int(L.pccl_staging_bytes(0 if kind == "ag" else 1, a, p, n, code)))
             combos = []
             for v in map(int, args.variants.split(",")):
-                if v >= 2 and algo != "direct":
+                if v in (2, 3, 4) and algo != "direct":
                     continue
                 if v >= 2 and kind == "rs":
+                    continue
+                if v == 5 and algo == "direct":  # copy engine: ring / recursive doubling all-gather
                     continue
                 for tm in (args.tma.split(",") if v >= 2 else ["0x0"]):
                     combos.append((v, *map(int, tm.split("x"))))
