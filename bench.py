@@ -373,6 +373,46 @@ def run_gpu(args):
                 extra["nccl_ag_f32_64MiB"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
                 del nin, nout, agi, ago
 
+            # the metric's range (64-256 MB): both collectives, every flat algorithm, at its ends
+            for S_r in (64 << 20, 256 << 20):
+                for coll, dt_r in (("ag", torch.float32), ("rs", torch.bfloat16)):
+                    es_r = torch.empty(0, dtype=dt_r).element_size()
+                    n_r = S_r // es_r // p
+                    code_r = _lib.DTYPES["f32" if dt_r == torch.float32 else "bf16"]
+                    c_in, c_out = (n_r, n_r * p) if coll == "ag" else (n_r * p, n_r)
+                    if real:
+                        r_in, r_out = world.empty(c_in, dt_r), world.empty(c_out, dt_r)
+                        r_in.normal_()
+                    else:
+                        r_ins, r_outs = world.empty(c_in, dt_r), world.empty(c_out, dt_r)
+                        for t_ in r_ins:
+                            t_.normal_()
+                        r_sp = _lib.ptr_array([t_.data_ptr() for t_ in r_ins])
+                        r_rp = _lib.ptr_array([t_.data_ptr() for t_ in r_outs])
+                    for alg2 in ("direct", "ring", "recursive"):
+                        a2 = _lib.ALGOS[alg2]
+                        o2 = _lib.ORDERS["recursive" if alg2 == "recursive" else "ring"]
+                        world.ensure_staging(int(L.pccl_staging_bytes(0 if coll == "ag" else 1, a2, p, n_r, code_r)))
+                        if coll == "ag" and real:
+                            f = lambda: _lib.check(L.pccl_all_gather(ghandle, a2, r_in.data_ptr(), r_out.data_ptr(),  # noqa: E731
+                                                                    n_r, code_r, stream.cuda_stream))
+                        elif coll == "ag":
+                            f = lambda: _lib.check(L.pccl_emu_all_gather(group.handle, a2, r_sp, r_rp, n_r, code_r,  # noqa: E731
+                                                                        stream.cuda_stream))
+                        elif real:
+                            f = lambda: _lib.check(L.pccl_reduce_scatter(ghandle, a2, o2, r_in.data_ptr(),  # noqa: E731
+                                                                        r_out.data_ptr(), n_r, code_r, stream.cuda_stream))
+                        else:
+                            f = lambda: _lib.check(L.pccl_emu_reduce_scatter(group.handle, a2, o2, r_sp, r_rp, n_r,  # noqa: E731
+                                                                            code_r, stream.cuda_stream))
+                        t = measure(f)
+                        tag = f"{coll}_{'f32' if coll == 'ag' else 'bf16'}_{S_r >> 20}MiB_{alg2}"
+                        extra[tag] = {"busbw_gbs": round(busbw(S_r, p, t), 1), "us": round(t * 1e6, 1)}
+                    if real:
+                        del r_in, r_out
+                    else:
+                        del r_ins, r_outs
+
             # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
             S_h = 256 << 20
             grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]

@@ -42,8 +42,12 @@ def main() -> int:
     dist.init_process_group("nccl", device_id=dev)
     import paper_2504_18658_b200 as pkg
 
+    from paper_2504_18658_b200 import _lib, collectives as C
+
     comm = pkg.init_from_torch(device=dev.index)
     w = comm.world
+    ce = bool(_lib.lib().pccl_ce_available(dev.index))
+    C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES = 64 << 10, 16 << 10  # host buffers: sliced path, many slices
     rng = random.Random(a.seed)  # same stream on every rank: SPMD calls
     pow2 = p & (p - 1) == 0
     grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
@@ -68,7 +72,9 @@ def main() -> int:
             n = max(1, n // p)
         algo = rng.choice(["direct", "ring"] + (["recursive"] if pow2 else []))
         order = rng.choice(["ring", "rank"] + (["recursive"] if pow2 else []))
-        kind = rng.choice(["sym", "plain", "misaligned"])
+        kind = rng.choice(["sym", "plain", "misaligned", "host"] if coll != "hier" else ["sym", "plain", "misaligned"])
+        w.set_param("item_kib", rng.choice([0, 0, 16, 64]))  # direct kernels: static slices / work items
+        w.set_param("ag_variant", rng.choice([-1, -1, 5] if ce else [-1]))  # 5: copy engine (ring / recursive)
         total_in = n if coll == "ag" else n * p
         total_out = n * p if coll == "ag" else n
         if kind == "sym":
@@ -76,10 +82,21 @@ def main() -> int:
         elif kind == "plain":
             x = torch.empty(total_in, dtype=dtype, device=dev)
             y = torch.empty(total_out, dtype=dtype, device=dev)
-        else:
+        elif kind == "misaligned":
             x = torch.empty(total_in + 2, dtype=dtype, device=dev)[1:1 + total_in]
             y = torch.empty(total_out + 2, dtype=dtype, device=dev)[1:1 + total_out]
+        else:  # pinned host input -> fresh host output (the reference-shaped path)
+            x = torch.empty(total_in, dtype=dtype, pin_memory=True)
+            y = None
         x.copy_(values(it, rank, 0, total_in, dtype, dev))
+        if kind == "host":
+            if coll == "ag":
+                y = pkg.all_gather(comm, x, algorithm=algo).to(dev)
+                want = torch.cat([values(it, q, 0, n, dtype, dev) for q in range(p)])
+            else:
+                y = pkg.reduce_scatter(comm, x, algorithm=algo, order=order).to(dev)
+                want = sum(values(it, q, rank * n, n, torch.float32, dev) for q in range(p)).to(dtype)
+            return y, want, f"{coll} {algo}/{order} {dtype} n={n} host"
         if coll == "ag":
             pkg.all_gather(comm, x, algorithm=algo, out=y)
             want = torch.cat([values(it, q, 0, n, dtype, dev) for q in range(p)])
@@ -110,6 +127,8 @@ def main() -> int:
 
     for it in range(a.iters):
         if it % 25 == 24:
+            w.set_param("ag_variant", -1)
+            w.set_param("item_kib", 0)
             # CUDA graph: capture three fixed calls on a side stream, replay, verify
             side = torch.cuda.Stream(dev)
             n = rng.choice([256, 8192, 1 << 18])
