@@ -188,10 +188,17 @@ def rs_algorithmic_hbm_bytes(algo: str, p: int, chunk_bytes: int) -> int:
 
 
 def time_calls(call, steps: int, stream) -> float:
-    """Average seconds per call over `steps` back-to-back calls on `stream`."""
+    """Average seconds per call over `steps` back-to-back calls on `stream`.
+
+    One untimed call goes first: it is a device-side rendezvous of all ranks,
+    so the start event is recorded when every rank's stream has reached the
+    timed region. Without it the slowest rank's host leaving the barrier late
+    (scheduling jitter, up to ~1 ms on these hosts) lands in the other ranks'
+    first timed call."""
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    call()
     e0.record(stream)
     for _ in range(steps):
         call()
