@@ -34,6 +34,19 @@ __global__ void k_mc_store(const uint4 *src, char *mc_dst, size_t n) {
   }
 }
 
+// each GPU reduces its chunk across all GPUs through the switch (bf16, 8 per 16 B)
+__global__ void k_mc_ld_reduce(const char *mc_src, uint4 *dst, size_t n) {
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint4 v;
+    const uint4 *s = reinterpret_cast<const uint4 *>(mc_src) + i;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(s)
+                 : "memory");
+    dst[i] = v;
+  }
+}
+
 __global__ void k_check(const uint4 *p, size_t n, uint32_t tag, unsigned long long *bad) {
   for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint4 v = p[i];
@@ -139,6 +152,31 @@ int main(int argc, char **argv) {
     printf("rep %d: %zu MiB/GPU multicast to %d GPUs in %.1f us -> ingress %.1f GB/s per GPU (ctas %d)\n", rep,
            bytes >> 20, ng, worst * 1e3, (double)bytes * (ng - 1) / (worst * 1e-3) / 1e9, ctas);
   }
+  // reduce-scatter through the switch: GPU g reads chunk g (bytes) of the
+  // multicast buffer with ld_reduce; busbw = (ng-1)/ng * (ng*bytes) / t
+  for (int rep = 0; rep < 3; ++rep) {
+    std::vector<cudaEvent_t> e0(ng), e1(ng);
+    for (int g = 0; g < ng; ++g) {
+      cudaSetDevice(g);
+      cudaEventCreate(&e0[g]);
+      cudaEventCreate(&e1[g]);
+      cudaEventRecord(e0[g], st[g]);
+      for (int it = 0; it < 10; ++it)
+        k_mc_ld_reduce<<<ctas, 512, 0, st[g]>>>((const char *)mcva[g] + (size_t)g * bytes, src[g], bytes / 16);
+      cudaEventRecord(e1[g], st[g]);
+    }
+    double worst = 0;
+    for (int g = 0; g < ng; ++g) {
+      cudaSetDevice(g);
+      cudaEventSynchronize(e1[g]);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0[g], e1[g]);
+      worst = ms / 10 > worst ? ms / 10 : worst;
+    }
+    printf("rep %d: ld_reduce bf16 chunk %zu MiB/GPU from %d GPUs in %.1f us -> RS busbw %.1f GB/s (ctas %d)\n", rep,
+           bytes >> 20, ng, worst * 1e3, (double)bytes * (ng - 1) / (worst * 1e-3) / 1e9, ctas);
+  }
+  for (int g = 0; g < ng; ++g) { cudaSetDevice(g); cudaDeviceSynchronize(); }
   unsigned long long *bad;
   cudaMallocManaged(&bad, 8);
   *bad = 0;
