@@ -39,6 +39,7 @@ import torch  # noqa: E402
 METRIC = "all-gather & reduce-scatter bus GB/s (64–256 MB) at 2/4/8 B200 vs 900 GB/s"
 NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (fallback; nominal 900)
 NVLINK_NOMINAL_GBS = 900.0
+PATTERN_CEILING_GBS = {"recursive": 642.0, "ring": 680.0, "direct": 634.0}  # profiles/r1_engine_probe_p4.md (rs ring pushes)
 EMU_RANKS = 8
 
 
@@ -500,6 +501,13 @@ def run_gpu(args):
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
                 "frac_of_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4),
+                # the traffic pattern's own measured ceiling (raw 16-byte loops, no flags, p=4,
+                # tools/probe.py / profiles/r1_engine_probe_p4.md): recursive halving and ring are
+                # pairwise bidirectional peer loads, direct is all-to-all peer loads
+                "pattern_ceiling": {"gbs": PATTERN_CEILING_GBS.get(algo), "frac": round(
+                    achieved / PATTERN_CEILING_GBS[algo], 4) if algo in PATTERN_CEILING_GBS else None,
+                    "source": "tools/probe.py raw loops at p=4: recursive = bidirectional LDG pull, ring = "
+                              "bidirectional STG push, direct = all-to-all LDG pull"},
                 "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
                 "algorithmic_bytes_per_launch": int(S * (p - 1) / p), "traffic": None}
     else:
