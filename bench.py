@@ -421,6 +421,37 @@ def run_gpu(args):
                     else:
                         del r_ins, r_outs
 
+            # NVLS: switch multicast stores (AG) / switch reductions (bf16 RS)
+            if real:
+                from paper_2504_18658_b200 import nvls as NV
+
+                if NV.nvls_supported(world):
+                    P7n = 12 * 4096 * 4096 + 13 * 4096
+                    seg = NV.create_nvls_segment(world, max(S, P7n * 2 + 4096))
+                    try:
+                        nx = seg.tensor(0, n * p, torch.bfloat16)
+                        nx.normal_()
+                        ny = torch.empty(n, dtype=torch.bfloat16, device=dev)
+                        t = measure(lambda: NV.nvls_reduce_scatter(comm, seg, nx, ny))
+                        extra[f"nvls_rs_bf16_{args.size_mib}MiB"] = {"busbw_gbs": round(busbw(S, p, t), 1),
+                                                                   "us": round(t * 1e6, 1)}
+                        for S_a, dt_a, nm in ((64 << 20, torch.float32, "ag_f32_64MiB"),
+                                              (P7n // p * p * 2, torch.bfloat16, "fsdp7b_layer_ag_bf16")):
+                            n_a = S_a // torch.empty(0, dtype=dt_a).element_size() // p
+                            ax = torch.empty(n_a, dtype=dt_a, device=dev).normal_()
+                            ay = seg.tensor(0, n_a * p, dt_a)
+                            t = measure(lambda: NV.nvls_all_gather(comm, seg, ax, ay))
+                            extra[f"nvls_{nm}"] = {"busbw_gbs": round(busbw(S_a, p, t), 1), "us": round(t * 1e6, 1)}
+                        n7 = P7n // p
+                        gx = seg.tensor(0, n7 * p, torch.bfloat16)
+                        gx.normal_()
+                        gy = torch.empty(n7, dtype=torch.bfloat16, device=dev)
+                        t = measure(lambda: NV.nvls_reduce_scatter(comm, seg, gx, gy))
+                        extra["nvls_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(n7 * p * 2, p, t), 1),
+                                                              "us": round(t * 1e6, 1)}
+                    finally:
+                        seg.close()
+
             # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
             S_h = 256 << 20
             grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]

@@ -195,6 +195,33 @@ int pccl_reduce_inplace(void *acc, const void *other, size_t count, int dtype, v
  * ring / recursive doubling into a registered (symmetric) output outside
  * stream capture, in real mode; any other call falls back to the kernels. */
 int pccl_ce_available(int device);
+
+/* NVLS (NVLink SHARP multicast) segments and collectives. A multicast
+ * segment is one switch multicast object spanning every device of the world,
+ * with each rank's physical memory bound to it and mapped twice (unicast:
+ * plain access to my copy; multicast: multimem ops). Setup is collective:
+ * one rank pccl_nvls_create()s the object and passes the returned POSIX file
+ * descriptor to the others (SCM_RIGHTS), which pccl_nvls_import() it; then
+ * every rank pccl_nvls_add_device(), a barrier, every rank pccl_nvls_bind().
+ * The collectives run over a world-spanning communicator; offsets, sizes
+ * and pointers must be 16-byte aligned. AG: each rank multicasts its block
+ * (multimem.st) into out_offset + g * count of every rank's copy. RS: each
+ * rank's input sits at in_offset of its copy; chunk g is read as the switch's
+ * sum over all copies (multimem.ld_reduce, fp32 accumulation for bf16 /
+ * fp16) and stored to recv. The switch's summation order is not the
+ * reference's, so the RS is for bf16 / fp16 training traffic, not for fp32
+ * order parity. */
+int pccl_nvls_supported(pccl_world_t w);
+int pccl_nvls_create(pccl_world_t w, size_t bytes, size_t *alloc_bytes, int *fd, int *nvls_id);
+int pccl_nvls_import(pccl_world_t w, int fd, size_t alloc_bytes, int *nvls_id);
+int pccl_nvls_add_device(pccl_world_t w, int nvls_id);
+int pccl_nvls_bind(pccl_world_t w, int nvls_id);
+int pccl_nvls_ptr(pccl_world_t w, int nvls_id, void **unicast, void **multicast, size_t *bytes);
+int pccl_nvls_destroy(pccl_world_t w, int nvls_id);
+int pccl_nvls_all_gather(pccl_comm_t c, int nvls_id, const void *send, size_t out_offset, size_t count, int dtype,
+                         void *stream);
+int pccl_nvls_reduce_scatter(pccl_comm_t c, int nvls_id, size_t in_offset, void *recv, size_t recvcount, int dtype,
+                             void *stream);
 int pccl_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height, void *stream);
 
 /* ---- schedule introspection (host only, no GPU needed) -------------------

@@ -66,6 +66,15 @@ _SIGS = {
     "pccl_reduce_inplace": (_i, [_vp, _vp, _sz, _i, _vp]),
     "pccl_copy2d": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _vp]),
     "pccl_ce_available": (_i, [_i]),
+    "pccl_nvls_supported": (_i, [_vp]),
+    "pccl_nvls_create": (_i, [_vp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
+    "pccl_nvls_import": (_i, [_vp, _i, _sz, ctypes.POINTER(_i)]),
+    "pccl_nvls_add_device": (_i, [_vp, _i]),
+    "pccl_nvls_bind": (_i, [_vp, _i]),
+    "pccl_nvls_ptr": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_sz)]),
+    "pccl_nvls_destroy": (_i, [_vp, _i]),
+    "pccl_nvls_all_gather": (_i, [_vp, _i, _vp, _sz, _sz, _i, _vp]),
+    "pccl_nvls_reduce_scatter": (_i, [_vp, _i, _sz, _vp, _sz, _i, _vp]),
     "pccl_schedule": (_i, [_i, _i, _i, _i, _i, _sz, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(_i)]),
 }
 

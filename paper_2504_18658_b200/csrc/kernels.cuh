@@ -862,6 +862,106 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant
   ll_finish(c, s_tag, code);
 }
 
+// ============================================================================
+// NVLS (NVLink SHARP) collectives through a multicast segment (variant 6).
+// P.recv (AG) / P.send (RS) hold this rank's *multicast* mapping of the
+// segment: a multimem.st there lands in every member's copy, a
+// multimem.ld_reduce returns the sum of every member's copy, both executed
+// by the NVSwitch. Accesses through the multicast and the unicast mapping of
+// the same memory are different proxies, hence fence.proxy.alias around the
+// flag handshakes.
+// ============================================================================
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+__device__ __forceinline__ void mc_st(uint4 *p, const uint4 &v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+template <int DT> __device__ __forceinline__ uint4 mc_ld_reduce(const uint4 *p);
+template <> __device__ __forceinline__ uint4 mc_ld_reduce<DT_BF16>(const uint4 *p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+template <> __device__ __forceinline__ uint4 mc_ld_reduce<DT_F16>(const uint4 *p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+template <> __device__ __forceinline__ uint4 mc_ld_reduce<DT_F32>(const uint4 *p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// All-gather: entry = "my output may be overwritten", then every rank
+// multicasts its block once, then "my block has landed everywhere".
+__global__ void __launch_bounds__(kThreads) k_nvls_ag(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
+  cta_signal_entry(c, peers);
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  fence_proxy_alias();
+  const uint4 *src = reinterpret_cast<const uint4 *>(P.send[c.r]);
+  uint4 *mc = reinterpret_cast<uint4 *>(P.recv[c.r]) + P.base[c.y] + (int64_t)c.gi * P.istride;
+  const int nt = blockDim.x;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (i + (int64_t)u * nt < hi) v[u] = __ldg(src + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (i + (int64_t)u * nt < hi) mc_st(mc + i + (int64_t)u * nt, v[u]);
+  }
+  fence_proxy_alias();
+  __threadfence_system();
+  cta_signal_mask(c, peers, 1);
+  if (!cta_wait_mask(c, peers, 1, false)) return;
+  fence_proxy_alias();
+}
+
+// Reduce-scatter: entry = "my input is in my copy of the segment", then
+// chunk gi is read through the switch as the sum over all members (fp32
+// accumulation for bf16 / fp16), exit = "I have finished reading yours".
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_nvls_rs(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
+  cta_signal_entry(c, peers);
+  int64_t lo, hi;
+  split32(P.blk, P.ctas, c.b, lo, hi);
+  if (!cta_wait_mask(c, peers, 0, true)) return;
+  fence_proxy_alias();
+  const uint4 *mc = reinterpret_cast<const uint4 *>(P.send[c.r]) + P.base[c.y] + (int64_t)c.gi * P.istride;
+  uint4 *dst = reinterpret_cast<uint4 *>(P.out[c.r]);
+  const int nt = blockDim.x;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (i + (int64_t)u * nt < hi) v[u] = mc_ld_reduce<DT>(mc + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (i + (int64_t)u * nt < hi) dst[i + (int64_t)u * nt] = v[u];
+  }
+  fence_proxy_alias();
+  cta_exit(c, peers, peers);
+}
+
 // TMA variant of the probe (modes 4 push / 5 pull): one thread per CTA moves
 // its range through a shared-memory ring with cp.async.bulk (bulk loads from
 // the source, bulk stores to the destination), the data path of the TMA

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 using namespace pccl;
@@ -50,6 +51,12 @@ struct pccl_world {
   int *err_dev = nullptr;
   uint64_t epoch[PCCL_NSLOTS] = {};
   uint64_t ce_calls[PCCL_NSLOTS] = {};  // copy-engine collectives per group (host-issued, never captured)
+  struct NvlsSeg {  // multicast segment (NVLS): this rank's physical memory bound to a switch multicast object
+    bool used = false, bound = false;
+    unsigned long long mc = 0, mem = 0;  // CUmemGenericAllocationHandle
+    unsigned long long mc_va = 0, uc_va = 0;
+    size_t bytes = 0, gran = 0;  // gran: multicast granularity (VA alignment of both mappings)
+  } nvls[4];
   std::map<uint32_t, int> slot_of_mask;  // emulation: dynamic slot allocation
   int sms = 148;
   // tuning knobs (pccl_world_set_param)
@@ -349,6 +356,13 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     int maxp = 2;
     while (maxp < pl.gs) maxp <<= 1;
     k = rs_kernel(pl.dtype, vec, pl.algo, pl.order, maxp, pl.variant);
+  }
+  if (pl.variant == 6) {  // NVLS: 16-byte vectors through the multicast mapping (caller checked alignment)
+    U = 16;
+    if (pl.coll == PCCL_ALL_GATHER) k = (KernelFn)k_nvls_ag;
+    else if (pl.dtype == PCCL_BFLOAT16) k = (KernelFn)k_nvls_rs<DT_BF16>;
+    else if (pl.dtype == PCCL_FLOAT16) k = (KernelFn)k_nvls_rs<DT_F16>;
+    else k = (KernelFn)k_nvls_rs<DT_F32>;
   }
   if (!k) return PCCL_ERR_UNSUPPORTED;
   const int64_t epu = U / (int64_t)es > 0 ? U / (int64_t)es : 1;  // elements per unit
@@ -664,6 +678,74 @@ int ce_all_gather(pccl_comm *c, int algo, const void *send, void *recv, size_t b
   }
 #undef CE
   return PCCL_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// NVLS multicast segments (driver VMM + multicast API through cudart's entry
+// points, so the library has no link-time dependency on libcuda).
+// --------------------------------------------------------------------------
+struct DrvNvls {
+  bool ok = false;
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle *, const CUmulticastObjectProp *);
+  CUresult (*mcGran)(size_t *, const CUmulticastObjectProp *, CUmulticastGranularity_flags);
+  CUresult (*mcAddDev)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*mcBind)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                     unsigned long long);
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*exportH)(void *, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+  CUresult (*importH)(CUmemGenericAllocationHandle *, void *, CUmemAllocationHandleType);
+  CUresult (*memCreate)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *, unsigned long long);
+  CUresult (*memRelease)(CUmemGenericAllocationHandle);
+  CUresult (*reserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*addrFree)(CUdeviceptr, size_t);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t);
+  CUresult (*attr)(int *, CUdevice_attribute, CUdevice);
+};
+
+DrvNvls &drv_nvls() {
+  static DrvNvls d;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    bool ok = true;
+    auto get = [&](const char *name, auto &fn) {
+      void *f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+          !f) {
+        cudaGetLastError();
+        ok = false;
+        return;
+      }
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(f);
+    };
+    get("cuMulticastCreate", d.mcCreate);
+    get("cuMulticastGetGranularity", d.mcGran);
+    get("cuMulticastAddDevice", d.mcAddDev);
+    get("cuMulticastBindMem", d.mcBind);
+    get("cuMulticastUnbind", d.mcUnbind);
+    get("cuMemExportToShareableHandle", d.exportH);
+    get("cuMemImportFromShareableHandle", d.importH);
+    get("cuMemCreate", d.memCreate);
+    get("cuMemRelease", d.memRelease);
+    get("cuMemAddressReserve", d.reserve);
+    get("cuMemAddressFree", d.addrFree);
+    get("cuMemMap", d.map);
+    get("cuMemUnmap", d.unmap);
+    get("cuMemSetAccess", d.setAccess);
+    get("cuDeviceGetAttribute", d.attr);
+    d.ok = ok;
+  });
+  return d;
+}
+
+CUmulticastObjectProp nvls_prop(const pccl_world *w, size_t bytes) {
+  CUmulticastObjectProp mp = {};
+  mp.numDevices = (unsigned)w->nranks;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = bytes;
+  return mp;
 }
 
 // --------------------------------------------------------------------------
@@ -1047,6 +1129,214 @@ int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::ve
 
 int pccl_ce_available(int device) { return memops(device).ok ? 1 : 0; }
 
+// ---- NVLS multicast segments and collectives --------------------------------
+#define CUD(x)                                                                  \
+  do {                                                                          \
+    const CUresult _r = (x);                                                    \
+    if (_r != CUDA_SUCCESS) {                                                   \
+      fprintf(stderr, "[pccl_b200] %s failed: CUresult %d\n", #x, (int)_r);     \
+      return PCCL_ERR_CUDA;                                                     \
+    }                                                                           \
+  } while (0)
+
+int pccl_nvls_supported(pccl_world_t w) {
+  if (!w || w->emu) return 0;
+  DrvNvls &d = drv_nvls();
+  if (!d.ok) return 0;
+  int v = 0;
+  if (d.attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, (CUdevice)w->device) != CUDA_SUCCESS) return 0;
+  return v ? 1 : 0;
+}
+
+static int nvls_slot(pccl_world *w) {
+  for (int i = 0; i < 4; ++i)
+    if (!w->nvls[i].used) return i;
+  return -1;
+}
+
+int pccl_nvls_create(pccl_world_t w, size_t bytes, size_t *alloc_bytes, int *fd, int *nvls_id) {
+  if (!w || !alloc_bytes || !fd || !nvls_id || bytes == 0) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!pccl_nvls_supported(w)) return PCCL_ERR_UNSUPPORTED;
+  DrvNvls &d = drv_nvls();
+  CK(cudaSetDevice(w->device));
+  CK(cudaFree(0));  // the primary context is current
+  const int id = nvls_slot(w);
+  if (id < 0) return PCCL_ERR_OUT_OF_MEMORY;
+  CUmulticastObjectProp mp = nvls_prop(w, bytes);
+  size_t gran = 0;
+  CUD(d.mcGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  mp.size = (bytes + gran - 1) / gran * gran;
+  CUmemGenericAllocationHandle mc;
+  CUD(d.mcCreate(&mc, &mp));
+  int h = -1;
+  if (d.exportH(&h, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS) {
+    d.memRelease(mc);
+    return PCCL_ERR_CUDA;
+  }
+  auto &S = w->nvls[id];
+  S = {};
+  S.used = true;
+  S.mc = mc;
+  S.bytes = mp.size;
+  S.gran = gran;
+  *alloc_bytes = mp.size;
+  *fd = h;
+  *nvls_id = id;
+  return PCCL_SUCCESS;
+}
+
+int pccl_nvls_import(pccl_world_t w, int fd, size_t alloc_bytes, int *nvls_id) {
+  if (!w || fd < 0 || !alloc_bytes || !nvls_id) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!pccl_nvls_supported(w)) return PCCL_ERR_UNSUPPORTED;
+  DrvNvls &d = drv_nvls();
+  CK(cudaSetDevice(w->device));
+  CK(cudaFree(0));
+  const int id = nvls_slot(w);
+  if (id < 0) return PCCL_ERR_OUT_OF_MEMORY;
+  CUmulticastObjectProp mp = nvls_prop(w, alloc_bytes);
+  size_t gran = 0;
+  CUD(d.mcGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemGenericAllocationHandle mc;
+  CUD(d.importH(&mc, (void *)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  auto &S = w->nvls[id];
+  S = {};
+  S.used = true;
+  S.mc = mc;
+  S.bytes = alloc_bytes;
+  S.gran = gran;
+  *nvls_id = id;
+  return PCCL_SUCCESS;
+}
+
+// Every rank adds its own device; all must have done so before any binds.
+int pccl_nvls_add_device(pccl_world_t w, int id) {
+  if (!w || id < 0 || id >= 4 || !w->nvls[id].used) return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  CUD(drv_nvls().mcAddDev((CUmemGenericAllocationHandle)w->nvls[id].mc, (CUdevice)w->device));
+  return PCCL_SUCCESS;
+}
+
+// Physical memory on my device, bound to the multicast object, mapped twice:
+// unicast (my copy, plain loads / stores) and multicast (multimem ops).
+int pccl_nvls_bind(pccl_world_t w, int id) {
+  if (!w || id < 0 || id >= 4 || !w->nvls[id].used || w->nvls[id].bound) return PCCL_ERR_INVALID_ARGUMENT;
+  DrvNvls &d = drv_nvls();
+  auto &S = w->nvls[id];
+  CK(cudaSetDevice(w->device));
+  CUmemAllocationProp ap = {};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = w->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmemGenericAllocationHandle mem;
+  CUD(d.memCreate(&mem, S.bytes, &ap, 0));
+  S.mem = mem;
+  CUD(d.mcBind((CUmemGenericAllocationHandle)S.mc, 0, mem, 0, S.bytes, 0));
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = w->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr uc = 0, mc = 0;
+  CUD(d.reserve(&uc, S.bytes, S.gran, 0, 0));
+  CUD(d.map(uc, S.bytes, 0, mem, 0));
+  CUD(d.setAccess(uc, S.bytes, &acc, 1));
+  CUD(d.reserve(&mc, S.bytes, S.gran, 0, 0));
+  CUD(d.map(mc, S.bytes, 0, (CUmemGenericAllocationHandle)S.mc, 0));
+  CUD(d.setAccess(mc, S.bytes, &acc, 1));
+  S.uc_va = uc;
+  S.mc_va = mc;
+  S.bound = true;
+  CK(cudaMemset((void *)uc, 0, S.bytes));
+  CK(cudaDeviceSynchronize());
+  return PCCL_SUCCESS;
+}
+
+int pccl_nvls_ptr(pccl_world_t w, int id, void **uc, void **mc, size_t *bytes) {
+  if (!w || id < 0 || id >= 4 || !w->nvls[id].bound) return PCCL_ERR_INVALID_ARGUMENT;
+  if (uc) *uc = (void *)w->nvls[id].uc_va;
+  if (mc) *mc = (void *)w->nvls[id].mc_va;
+  if (bytes) *bytes = w->nvls[id].bytes;
+  return PCCL_SUCCESS;
+}
+
+int pccl_nvls_destroy(pccl_world_t w, int id) {
+  if (!w || id < 0 || id >= 4 || !w->nvls[id].used) return PCCL_ERR_INVALID_ARGUMENT;
+  DrvNvls &d = drv_nvls();
+  auto &S = w->nvls[id];
+  cudaSetDevice(w->device);
+  cudaDeviceSynchronize();
+  if (S.mc_va) { d.unmap(S.mc_va, S.bytes); d.addrFree(S.mc_va, S.bytes); }
+  if (S.uc_va) { d.unmap(S.uc_va, S.bytes); d.addrFree(S.uc_va, S.bytes); }
+  if (S.bound) d.mcUnbind((CUmemGenericAllocationHandle)S.mc, (CUdevice)w->device, 0, S.bytes);
+  if (S.mem) d.memRelease((CUmemGenericAllocationHandle)S.mem);
+  if (S.mc) d.memRelease((CUmemGenericAllocationHandle)S.mc);
+  S = {};
+  return PCCL_SUCCESS;
+}
+
+// Collectives over a world-spanning communicator (the multicast object spans
+// every device of the world). AG: send anywhere on my device, output at
+// out_offset of the segment (every rank's copy); RS: input at in_offset of
+// the segment (my copy, written before the call), output anywhere.
+static int nvls_check(pccl_comm *c, int id, size_t off, size_t bytes_total, const void *p, size_t blk_bytes) {
+  pccl_world *w = c ? c->w : nullptr;
+  if (!w || w->emu || id < 0 || id >= 4 || !w->nvls[id].bound) return PCCL_ERR_INVALID_ARGUMENT;
+  if (c->gs != w->nranks) return PCCL_ERR_UNSUPPORTED;
+  if ((off | blk_bytes | (size_t)(uintptr_t)p) & 15) return PCCL_ERR_INVALID_ARGUMENT;
+  if (off + bytes_total > w->nvls[id].bytes) return PCCL_ERR_INVALID_ARGUMENT;
+  return check_world_err(w);
+}
+
+int pccl_nvls_all_gather(pccl_comm_t c, int id, const void *send, size_t out_offset, size_t count, int dtype,
+                         void *stream) {
+  const size_t es = dt_size(dtype);
+  if (!es) return PCCL_ERR_INVALID_ARGUMENT;
+  int st = nvls_check(c, id, out_offset, (size_t)(c ? c->gs : 0) * count * es, send, count * es);
+  if (st) return st;
+  if (count == 0) return PCCL_SUCCESS;
+  pccl_world *w = c->w;
+  CK(cudaSetDevice(w->device));
+  const int me = w->rank;
+  Plan pl;
+  pl.coll = PCCL_ALL_GATHER;
+  pl.algo = A_DIRECT;
+  pl.dtype = dtype;
+  pl.count = count;
+  pl.gs = c->gs;
+  pl.blk = pl.istride = pl.send_sub_stride = (int64_t)count;
+  pl.variant = 6;
+  pl.rows.push_back({me, c});
+  pl.send[me] = (char *)send;
+  pl.recv[me] = (char *)w->nvls[id].mc_va + out_offset;
+  pl.out[me] = (char *)w->nvls[id].uc_va + out_offset;
+  return launch(w, pl, (cudaStream_t)stream);
+}
+
+int pccl_nvls_reduce_scatter(pccl_comm_t c, int id, size_t in_offset, void *recv, size_t recvcount, int dtype,
+                             void *stream) {
+  if (dtype != PCCL_FLOAT32 && dtype != PCCL_BFLOAT16 && dtype != PCCL_FLOAT16) return PCCL_ERR_UNSUPPORTED;
+  const size_t es = dt_size(dtype);
+  int st = nvls_check(c, id, in_offset, (size_t)(c ? c->gs : 0) * recvcount * es, recv, recvcount * es);
+  if (st) return st;
+  if (recvcount == 0) return PCCL_SUCCESS;
+  pccl_world *w = c->w;
+  CK(cudaSetDevice(w->device));
+  const int me = w->rank;
+  Plan pl;
+  pl.coll = PCCL_REDUCE_SCATTER;
+  pl.algo = A_DIRECT;
+  pl.dtype = dtype;
+  pl.count = recvcount;
+  pl.gs = c->gs;
+  pl.blk = pl.istride = pl.out_sub_stride = (int64_t)recvcount;
+  pl.variant = 6;
+  pl.rows.push_back({me, c});
+  pl.send[me] = (char *)w->nvls[id].mc_va + in_offset;
+  pl.out[me] = (char *)recv;
+  return launch(w, pl, (cudaStream_t)stream);
+}
+#undef CUD
+
 
 // ============================================================================
 // C ABI
@@ -1131,6 +1421,8 @@ int pccl_world_destroy(pccl_world_t w) {
   cudaSetDevice(w->device);
   cudaDeviceSynchronize();
   for (auto &kv : w->comm_cache) delete kv.second;
+  for (int i = 0; i < 4; ++i)
+    if (w->nvls[i].used) pccl_nvls_destroy(w, i);
   for (int s = kMaxSegs - 1; s >= 0; --s)
     if (w->segs[s].used) pccl_segment_destroy(w, s);
   if (w->err_host) cudaFreeHost((void *)w->err_host);

@@ -95,6 +95,45 @@ def main() -> int:
             check(f"ce_ag_inplace_n{n}", out.cpu().numpy(), want)
         w.set_param("ag_variant", -1)
     sync_point("copy_engine")
+    # NVLS multicast segment (switch-executed AG stores / RS loads)
+    from paper_2504_18658_b200 import nvls as NV
+
+    if NV.nvls_supported(comm.world):
+        seg = NV.create_nvls_segment(comm.world, 16 << 20)
+        try:
+            for n in (8, 4096, 300_000):
+                for dt in (torch.float32, torch.bfloat16):
+                    ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+                    xs = [torch.from_numpy(a).to(dt) for a in ag_in]
+                    out = seg.tensor(0, n * p, dt)
+                    for _ in range(2):
+                        out.fill_(float("nan"))
+                        NV.nvls_all_gather(comm, seg, xs[rank].cuda(), out)
+                        check(f"nvls_ag_{dt}_n{n}", out.cpu().view(torch.uint8).numpy(),
+                              torch.cat(xs).view(torch.uint8).numpy())
+                    # RS: integer-valued inputs are exact in any summation order
+                    vals = [torch.from_numpy(rng.integers(-30, 31, n * p).astype(np.float32)).to(dt) for _ in range(p)]
+                    x = seg.tensor(1 << 20, n * p, dt)
+                    x.copy_(vals[rank])
+                    y = torch.empty(n, dtype=dt, device="cuda")
+                    for _ in range(2):
+                        NV.nvls_reduce_scatter(comm, seg, x, y)
+                        want = sum(v.float() for v in vals)[rank * n:(rank + 1) * n].to(dt)
+                        check(f"nvls_rs_{dt}_n{n}", y.cpu().float().numpy(), want.float().numpy())
+            # bf16 standard normal: fp32 accumulation in the switch, one rounding
+            n = 65536
+            vals = [torch.randn(n * p, generator=torch.Generator().manual_seed(q)).to(torch.bfloat16) for q in range(p)]
+            x = seg.tensor(1 << 20, n * p, torch.bfloat16)
+            x.copy_(vals[rank])
+            y = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            NV.nvls_reduce_scatter(comm, seg, x, y)
+            ref = sum(v.float() for v in vals)[rank * n:(rank + 1) * n]
+            bound = p * 2.0 ** -8 * sum(v.float().abs() for v in vals)[rank * n:(rank + 1) * n]
+            if not bool(((y.cpu().float() - ref).abs() <= bound).all()):
+                failures.append("nvls_rs_bf16_normal_bound")
+        finally:
+            seg.close()
+    sync_point("nvls")
     # pipelined host path (slices of every chunk / block, copies overlapped
     # with the collectives): small slice size so several slices run
     from paper_2504_18658_b200 import collectives as C
