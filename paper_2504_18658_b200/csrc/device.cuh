@@ -504,7 +504,10 @@ __device__ __forceinline__ void cta_subslice(const Ctx &c, int t, int64_t &lo, i
 // prefetches its next claim while moving the current item. The flag protocol
 // is unchanged: CTA b still signals / waits on the peers' CTA b, and since a
 // rank's kernel completes only after all of its CTAs' waits, the union over
-// b still covers every item of every peer.
+// b still covers every item of every peer — which is enough only where the
+// moved data is consumed after the launch (AG push) or was ready before it
+// (pull reads of the peers' inputs). Data pushed and consumed inside one
+// launch (RS direct push: push, then fold) keeps static slices.
 template <typename F>
 __device__ __forceinline__ void for_items(const Ctx &c, int64_t total, F &&body) {
   __shared__ long long s_item[2];

@@ -582,22 +582,13 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   split32(P.blk, P.ctas, c.b, lo, hi);
   const T *own = reinterpret_cast<const T *>(P.send[c.r]);
   if (PUSH) {
-    if (P.item > 0) {  // items (range j, destination i), destination fastest
-      const int nd = gs - 1;
-      const int64_t nj = (P.blk + P.item - 1) / P.item;
-      for_items(c, nj * nd, [&](int64_t id) {
-        const int64_t j = id / nd;
-        const int q = (gi + 1 + (int)(id - j * nd)) % gs;
-        const int64_t a = j * P.item, e = min(a + P.item, P.blk);
-        copy_typed<T>(reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk,
-                      own + P.base[c.y] + (int64_t)q * P.istride, a, e);
-      });
-    } else {
-      for (int i = 1; i < gs; ++i) {
-        const int q = (gi + i) % gs;
-        T *dst = reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk;
-        copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
-      }
+    // Static slices only: the fold below consumes, inside this launch, exactly
+    // the slice that the peers' CTA b pushed and signalled to my CTA b, so
+    // the push may not be redistributed by work items (P.item is ignored).
+    for (int i = 1; i < gs; ++i) {
+      const int q = (gi + i) % gs;
+      T *dst = reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk;
+      copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
     }
     cta_signal_mask(c, peers, 1);  // my chunks have landed
     if (!cta_wait_mask(c, peers, 1, false)) return;

@@ -48,6 +48,9 @@ def main() -> int:
     w = comm.world
     ce = bool(_lib.lib().pccl_ce_available(dev.index))
     C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES = 64 << 10, 16 << 10  # host buffers: sliced path, many slices
+    from paper_2504_18658_b200 import nvls as NV
+
+    seg = NV.create_nvls_segment(w, 64 << 20) if NV.nvls_supported(w) else None
     rng = random.Random(a.seed)  # same stream on every rank: SPMD calls
     pow2 = p & (p - 1) == 0
     grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
@@ -65,6 +68,23 @@ def main() -> int:
 
     def one_call(it):
         coll = rng.choice(["ag", "rs", "rs", "hier"] if grids else ["ag", "rs"])
+        if rng.random() < 0.15:  # NVLS (switch multicast) on the same world group, interleaved
+            dtype = rng.choice(DTYPES)
+            n = rng.choice([8, 1000, 40000, 1 << 18])
+            if seg is None:
+                return torch.zeros(1), torch.zeros(1), "nvls unsupported"
+            if rng.random() < 0.5:
+                x = values(it, rank, 0, n, dtype, dev)
+                y = seg.tensor(1 << 20, n * p, dtype)
+                NV.nvls_all_gather(comm, seg, x, y)
+                want = torch.cat([values(it, q, 0, n, dtype, dev) for q in range(p)])
+                return y.clone(), want, f"nvls ag {dtype} n={n}"
+            x = seg.tensor(1 << 20, n * p, dtype)
+            x.copy_(values(it, rank, 0, n * p, dtype, dev))
+            y = torch.empty(n, dtype=dtype, device=dev)
+            NV.nvls_reduce_scatter(comm, seg, x, y)
+            want = sum(values(it, q, rank * n, n, torch.float32, dev) for q in range(p)).to(dtype)
+            return y, want, f"nvls rs {dtype} n={n}"
         dtype = rng.choice(DTYPES)
         es = torch.empty(0, dtype=dtype).element_size()
         n = rng.choice([1, 3, 64, 1000, 4096, 40000, 262144, 1 << 20, (4 << 20) // es])
@@ -163,6 +183,8 @@ def main() -> int:
             w.check()
     torch.cuda.synchronize()
     w.check()
+    if seg is not None:
+        seg.close()
     eps = [None] * p
     dist.all_gather_object(eps, comm.epoch())
     if len(set(eps)) != 1:
