@@ -422,10 +422,17 @@ def run_gpu(args):
                         del r_ins, r_outs
 
             # NVLS: switch multicast stores (AG) / switch reductions (bf16 RS)
+            nvls_ok = real
             if real:
                 from paper_2504_18658_b200 import nvls as NV
 
-                if NV.nvls_supported(world):
+                try:
+                    nvls_ok = NV.nvls_supported(world)
+                except Exception as exc:  # noqa: BLE001 - optional path, never costs the rest
+                    extra["nvls_error"] = f"{type(exc).__name__}: {exc}"[:200]
+                    nvls_ok = False
+            if nvls_ok:
+                try:
                     P7n = 12 * 4096 * 4096 + 13 * 4096
                     seg = NV.create_nvls_segment(world, max(S, P7n * 2 + 4096))
                     try:
@@ -451,6 +458,9 @@ def run_gpu(args):
                                                               "us": round(t * 1e6, 1)}
                     finally:
                         seg.close()
+                except Exception as exc:  # noqa: BLE001 - optional path, never costs the rest
+                    extra["nvls_error"] = f"{type(exc).__name__}: {exc}"[:200]
+                    world.check()  # a device error (poisoned world) still ends the extras
 
             # C3: hierarchical AG + RS, 256 MiB, virtual N x M groupings
             S_h = 256 << 20

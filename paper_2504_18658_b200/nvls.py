@@ -102,6 +102,7 @@ def create_nvls_segment(world, nbytes: int) -> NvlsSegment:
             srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
             srv.bind(path)
             srv.listen(world.nranks)
+            srv.settimeout(120.0)  # a rank that never connects fails the setup instead of hanging it
             me = {"ok": True, "path": path, "alloc": alloc.value}
         else:
             me = {"ok": False, "why": _lib.error_string(st)}
@@ -116,6 +117,7 @@ def create_nvls_segment(world, nbytes: int) -> NvlsSegment:
                     socket.send_fds(conn, [b"f"], [fd.value])
         else:
             cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.settimeout(120.0)
             for _ in range(200):  # the server is listening before the exchange returned
                 try:
                     cli.connect(info["path"])

@@ -422,3 +422,16 @@ def test_param_validation():
             w.set_param(key, old)
     with pytest.raises(ValueError):
         w.set_param("no_such_knob", 1)
+
+
+def test_nvls_needs_real_mode():
+    """NVLS segments are a real-mode (one process per GPU) feature: an
+    emulated world reports no support and refuses to create one."""
+    pkg = _pkg()
+    from paper_2504_18658_b200 import nvls
+    from paper_2504_18658_b200.errors import Unsupported
+
+    w = pkg.emulated_world(2)
+    assert not nvls.nvls_supported(w)
+    with pytest.raises(Unsupported):
+        nvls.create_nvls_segment(w, 1 << 20)
