@@ -189,3 +189,37 @@ def test_bootstrap_exchange_world_size_2_gloo():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, [0, 1], True), (1, [0, 1], True)]
+
+
+# ---------------------------------------------------------------------------
+# sliced host-buffer path: slice geometry (collectives._pipeline_slices)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("row_len,es", [(1, 4), (1000, 4), (262144, 4), (300_007, 2), (1 << 24, 2), (5_000_011, 1),
+                                        (33_554_432, 4)])
+def test_pipeline_slices_cover_rows_exactly(row_len, es):
+    from paper_2504_18658_b200 import collectives as C
+
+    for in_bytes in (row_len * es, row_len * es * 8):
+        sl = C._pipeline_slices(row_len, es, in_bytes)
+        if in_bytes < C.PIPE_MIN_BYTES:
+            assert sl is None
+            continue
+        if sl is None:  # a row too short to split
+            assert row_len * es <= 256
+            continue
+        assert 2 <= len(sl) <= C.PIPE_MAX_SLICES
+        assert sl[0][0] == 0 and sum(n for _, n in sl) == row_len
+        for (a, n), (b, _) in zip(sl, sl[1:]):
+            assert a + n == b  # contiguous, no overlap
+        assert all((off * es) % 256 == 0 for off, _ in sl)  # vector-aligned slice starts
+        assert all(n > 0 for _, n in sl)
+
+
+def test_pipeline_slices_follow_the_size_knobs(monkeypatch):
+    from paper_2504_18658_b200 import collectives as C
+
+    monkeypatch.setattr(C, "PIPE_MIN_BYTES", 1 << 20)
+    monkeypatch.setattr(C, "PIPE_SLICE_BYTES", 1 << 20)
+    assert C._pipeline_slices(1 << 18, 4, (1 << 20) - 4) is None  # below the threshold
+    assert len(C._pipeline_slices(1 << 18, 4, 4 << 20)) == 4
+    assert len(C._pipeline_slices(1 << 24, 4, 1 << 30)) == C.PIPE_MAX_SLICES  # capped
