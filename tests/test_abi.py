@@ -2,7 +2,6 @@
 declares, maps status codes to the reference's exceptions, and its host-only
 step tables (the structure the kernels execute) equal the reference
 simulator's schedules (pkg/tests/test_acceptance.py:229-281)."""
-import ctypes
 import os
 import re
 

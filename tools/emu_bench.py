@@ -2,7 +2,7 @@
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-import paper_2504_18658_b200 as pkg
+import paper_2504_18658_b200  # noqa: F401  (loads the library)
 from paper_2504_18658_b200 import _lib
 from paper_2504_18658_b200.communicator import emulated_world, _emu_group
 
