@@ -917,8 +917,9 @@ __global__ void __launch_bounds__(kThreads) k_nvls_ag(const __grid_constant__ La
     for (int u = 0; u < kUnroll; ++u)
       if (i + (int64_t)u * nt < hi) mc_st(mc + i + (int64_t)u * nt, v[u]);
   }
+  // every thread orders its multicast stores (proxy fence); the CTA barrier
+  // plus the system-scope release of the "landed" flags publishes them
   fence_proxy_alias();
-  __threadfence_system();
   cta_signal_mask(c, peers, 1);
   if (!cta_wait_mask(c, peers, 1, false)) return;
   fence_proxy_alias();
