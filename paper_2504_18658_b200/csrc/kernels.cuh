@@ -624,35 +624,35 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
       }
 #pragma unroll
       for (int u = 0; u < EU; ++u) {
-      const int64_t e = e0 + (int64_t)u * nt;
-      if (e >= hi) break;
-      const T *raw = rawu[u];
-      Acc acc;
-      if (ORDER == O_REC) {
-        Acc v[MAXP];
+        const int64_t e = e0 + (int64_t)u * nt;
+        if (e >= hi) break;
+        const T *raw = rawu[u];
+        Acc acc;
+        if (ORDER == O_REC) {
+          Acc v[MAXP];
 #pragma unroll
-        for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
+          for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
 #pragma unroll
-        for (int h = MAXP / 2; h >= 1; h >>= 1) {
-          if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
+          for (int h = MAXP / 2; h >= 1; h >>= 1) {
+            if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
 #pragma unroll
-            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+              for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+            }
           }
+          acc = v[0];
+        } else if (ORDER == O_RANK) {
+#pragma unroll
+          for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+          for (int i = 0; i < MAXP; ++i)
+            if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+        } else {
+          acc = R::load(raw[0]);
+#pragma unroll
+          for (int i = 1; i < MAXP; ++i)
+            if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
         }
-        acc = v[0];
-      } else if (ORDER == O_RANK) {
-#pragma unroll
-        for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < MAXP; ++i)
-          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
-      } else {
-        acc = R::load(raw[0]);
-#pragma unroll
-        for (int i = 1; i < MAXP; ++i)
-          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
-      }
-      dst[e] = R::store(acc);
+        dst[e] = R::store(acc);
       }
     }
   };
