@@ -215,14 +215,24 @@ def run_gpu(args):
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    real = world_size > 1
+    # more ranks than GPUs (a functional check of the N-rank path on a smaller
+    # box: ranks time-share GPUs, bootstrap over gloo, no NCCL / NVLS extras;
+    # the numbers are not performance numbers)
+    shared = real and world_size > torch.cuda.device_count()
+    if shared:
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    real = world_size > 1
+    red_dev = torch.device("cpu") if shared else dev  # where max-over-ranks reductions live
     dist = None
     if real:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     p = world_size if real else EMU_RANKS
     S = args.size_mib << 20
     dtype = {"bf16": torch.bfloat16, "f32": torch.float32}[args.dtype]
@@ -295,7 +305,7 @@ def run_gpu(args):
                 call()
             t_est = time_calls(call, 5, stream)
             if real:
-                tt = torch.tensor([t_est], device=dev, dtype=torch.float64)
+                tt = torch.tensor([t_est], device=red_dev, dtype=torch.float64)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t_est = float(tt.item())
             for i in range(max(20, min(60000, int(3.0 / max(t_est, 1e-6))))):
@@ -310,7 +320,7 @@ def run_gpu(args):
         world.check()
         barrier()
     if real:
-        tt = torch.tensor([t_call], device=dev, dtype=torch.float64)
+        tt = torch.tensor([t_call], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_call = float(tt.item())
     value = busbw(S, p, t_call)
@@ -326,7 +336,7 @@ def run_gpu(args):
                 t = time_calls(fn, k, stream)
                 world.check()
                 if real:
-                    tt = torch.tensor([t], device=dev, dtype=torch.float64)
+                    tt = torch.tensor([t], device=red_dev, dtype=torch.float64)
                     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                     t = float(tt.item())
                 return t
@@ -367,7 +377,7 @@ def run_gpu(args):
                                                                 stream.cuda_stream))
                 t = measure(f)
                 extra[f"ag_f32_64MiB_{alg2}"] = {"busbw_gbs": round(busbw(S_ag, p, t), 1), "us": round(t * 1e6, 1)}
-            if real:
+            if real and not shared:
                 nin = torch.empty(n * p, dtype=dtype, device=dev).normal_()
                 nout = torch.empty(n, dtype=dtype, device=dev)
                 t = measure(lambda: dist.reduce_scatter_tensor(nout, nin))
@@ -421,8 +431,8 @@ def run_gpu(args):
                         del r_ins, r_outs
 
             # NVLS: switch multicast stores (AG) / switch reductions (bf16 RS)
-            nvls_ok = real
-            if real:
+            nvls_ok = real and not shared
+            if nvls_ok:
                 from paper_2504_18658_b200 import nvls as NV
 
                 try:
@@ -513,14 +523,17 @@ def run_gpu(args):
                 t = measure(lambda: pkg.reduce_scatter_tensor(gsh, grad, comm))
                 extra["fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1),
                                                  "bytes_in": S7, "algorithm": pkg.choose_algorithm("reduce_scatter", p, S7)}
-                nfull = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev)
-                nprm = torch.empty(n7, dtype=torch.bfloat16, device=dev).normal_()
-                t = measure(lambda: dist.all_gather_into_tensor(nfull, nprm))
-                extra["nccl_fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
-                ngrad = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev).normal_()
-                t = measure(lambda: dist.reduce_scatter_tensor(nprm, ngrad))
-                extra["nccl_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1), "us": round(t * 1e6, 1)}
-                del nfull, nprm, ngrad
+                if not shared:
+                    nfull = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev)
+                    nprm = torch.empty(n7, dtype=torch.bfloat16, device=dev).normal_()
+                    t = measure(lambda: dist.all_gather_into_tensor(nfull, nprm))
+                    extra["nccl_fsdp7b_layer_ag_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1),
+                                                          "us": round(t * 1e6, 1)}
+                    ngrad = torch.empty(n7 * p, dtype=torch.bfloat16, device=dev).normal_()
+                    t = measure(lambda: dist.reduce_scatter_tensor(nprm, ngrad))
+                    extra["nccl_fsdp7b_layer_rs_bf16"] = {"busbw_gbs": round(busbw(S7, p, t), 1),
+                                                          "us": round(t * 1e6, 1)}
+                    del nfull, nprm, ngrad
         except Exception as exc:  # an extra must never cost the headline line
             extra["error"] = f"{type(exc).__name__}: {exc}"[:300]
             if rank == 0:
@@ -590,7 +603,9 @@ def run_gpu(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": args.dtype,
-            "data": "synthetic (standard normal, resident in symmetric HBM segments)",
+            "data": "synthetic (standard normal, resident in symmetric HBM segments)"
+                    + ("; SHARED GPUS (more ranks than GPUs): functional check, not a performance number" if shared
+                       else ""),
             "config": {
                 "workload": (f"reduce-scatter {args.dtype}, {args.size_mib} MiB input/rank, {algo} "
                              f"(fused reduction), p={p} " + ("GPUs over NVLink/NVSwitch" if real else
@@ -637,7 +652,7 @@ def run_e2e(args, pkg, real, p, S, dtype, dev, comm, dist):
             t0 = time.perf_counter()
             y = fn(comm, x)
             per.append(time.perf_counter() - t0)
-        tt = torch.tensor(per, device=dev, dtype=torch.float64)
+        tt = torch.tensor(per, device="cpu" if dist.get_backend() == "gloo" else dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # per step: the slowest rank
         per = tt.tolist()
         h2d, d2h = n * p * es * p, n * es * p
