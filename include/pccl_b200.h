@@ -105,7 +105,8 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
 /* Tuning knobs by name: "ctas" (CTAs per rank, 0 = auto), "threads" (per
  * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
  * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL, 5 copy engine (AG ring /
- * recursive doubling, see pccl_ce_available)), "tma_stages",
+ * recursive doubling, see pccl_ce_available) / pipelined push with pusher and folder CTAs (RS
+ * direct)), "tma_stages",
  * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
  * collectives use the LL protocol — flags inside 16-byte data words, no
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /

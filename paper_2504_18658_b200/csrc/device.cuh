@@ -294,11 +294,12 @@ __device__ __forceinline__ bool cta_wait(Ctx &c, int m, int unit, bool check_met
 }
 
 // CTA-wide: wait for every member in `mask` (bit m) to complete `unit`.
-__device__ __forceinline__ bool cta_wait_mask(Ctx &c, uint32_t mask, int unit, bool check_meta = true) {
+// `idx`: the writers' CTA index whose words to wait on (default: mine).
+__device__ __forceinline__ bool cta_wait_mask(Ctx &c, uint32_t mask, int unit, bool check_meta = true, int idx = -1) {
   (void)check_meta;
   int code = 0;
   const int m = threadIdx.x;
-  if (m < c.gs && ((mask >> m) & 1u)) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, c.b), unit);
+  if (m < c.gs && ((mask >> m) & 1u)) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, idx < 0 ? c.b : idx), unit);
   int ok = __syncthreads_and(code == 0);
   if (!ok) {
     __shared__ int s_code;

@@ -566,11 +566,65 @@ __device__ __forceinline__ void copy_typed(T *d, const T *s, int64_t lo, int64_t
   for (; i < hi; i += nt) d[i] = __ldg(s + i);
 }
 
+// Fold the MAXP leaves src[i][off + e] of every element e in [lo, hi) in the
+// named order (registers only, fp32 accumulation) and store to dst[e].
+template <int DT, bool VEC, int ORDER, int MAXP>
+__device__ __forceinline__ void rs_fold(const typename RUnit<DT, VEC>::T *const *src, int gs, int64_t off,
+                                        typename RUnit<DT, VEC>::T *dst, int64_t lo, int64_t hi) {
+  using R = RUnit<DT, VEC>;
+  using T = typename R::T;
+  using Acc = typename R::Acc;
+  const int nt = blockDim.x;
+  // EU elements per thread per iteration keep >= 8 independent 16-byte
+  // loads in flight also for small groups (p = 2: 2 leaves per element)
+  constexpr int EU = MAXP >= 8 ? 1 : 8 / MAXP;
+  for (int64_t e0 = lo + threadIdx.x; e0 < hi; e0 += (int64_t)EU * nt) {
+    T rawu[EU][MAXP];
+#pragma unroll
+    for (int u = 0; u < EU; ++u) {
+      const int64_t e = e0 + (int64_t)u * nt;
+#pragma unroll
+      for (int i = 0; i < MAXP; ++i) rawu[u][i] = (i < gs && e < hi) ? ld_peer(src[i] + off + e) : T{};
+    }
+#pragma unroll
+    for (int u = 0; u < EU; ++u) {
+      const int64_t e = e0 + (int64_t)u * nt;
+      if (e >= hi) break;
+      const T *raw = rawu[u];
+      Acc acc;
+      if (ORDER == O_REC) {
+        Acc v[MAXP];
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
+#pragma unroll
+        for (int h = MAXP / 2; h >= 1; h >>= 1) {
+          if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
+#pragma unroll
+            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+          }
+        }
+        acc = v[0];
+      } else if (ORDER == O_RANK) {
+#pragma unroll
+        for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      } else {
+        acc = R::load(raw[0]);
+#pragma unroll
+        for (int i = 1; i < MAXP; ++i)
+          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+      }
+      dst[e] = R::store(acc);
+    }
+  }
+}
+
 template <int DT, bool VEC, int ORDER, int MAXP, bool PUSH>
 __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ LaunchParams P) {
   using R = RUnit<DT, VEC>;
   using T = typename R::T;
-  using Acc = typename R::Acc;
   Ctx c = make_ctx(P);
   CtaEpilogue fin(c);
   const int gs = c.gs, gi = c.gi;
@@ -607,54 +661,9 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
     else
       src[i] = reinterpret_cast<const T *>(P.send[c.world(q)]) + P.base[c.y] + (int64_t)gi * P.istride;
   }
-  const int nt = blockDim.x;
   auto fold = [&](int j, int64_t lo, int64_t hi) {
-    const int64_t off = (int64_t)j * P.sub_stride;
-    T *dst = reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride;
-    // EU elements per thread per iteration keep >= 8 independent 16-byte
-    // loads in flight also for small groups (p = 2: 2 leaves per element)
-    constexpr int EU = MAXP >= 8 ? 1 : 8 / MAXP;
-    for (int64_t e0 = lo + threadIdx.x; e0 < hi; e0 += (int64_t)EU * nt) {
-      T rawu[EU][MAXP];
-#pragma unroll
-      for (int u = 0; u < EU; ++u) {
-        const int64_t e = e0 + (int64_t)u * nt;
-#pragma unroll
-        for (int i = 0; i < MAXP; ++i) rawu[u][i] = (i < gs && e < hi) ? ld_peer(src[i] + off + e) : T{};
-      }
-#pragma unroll
-      for (int u = 0; u < EU; ++u) {
-        const int64_t e = e0 + (int64_t)u * nt;
-        if (e >= hi) break;
-        const T *raw = rawu[u];
-        Acc acc;
-        if (ORDER == O_REC) {
-          Acc v[MAXP];
-#pragma unroll
-          for (int i = 0; i < MAXP; ++i) v[i] = R::load(raw[i]);
-#pragma unroll
-          for (int h = MAXP / 2; h >= 1; h >>= 1) {
-            if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
-#pragma unroll
-              for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
-            }
-          }
-          acc = v[0];
-        } else if (ORDER == O_RANK) {
-#pragma unroll
-          for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
-#pragma unroll
-          for (int i = 0; i < MAXP; ++i)
-            if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
-        } else {
-          acc = R::load(raw[0]);
-#pragma unroll
-          for (int i = 1; i < MAXP; ++i)
-            if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
-        }
-        dst[e] = R::store(acc);
-      }
-    }
+    rs_fold<DT, VEC, ORDER, MAXP>(src, gs, (int64_t)j * P.sub_stride,
+                                  reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride, lo, hi);
   };
   if (!PUSH && P.item > 0) {  // pull: items (range, sub-block)
     const int64_t nj = (P.blk + P.item - 1) / P.item;
@@ -669,6 +678,64 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   if (!PUSH) cta_exit(c, peers, peers);
 }
 
+
+// Direct reduce-scatter, pipelined push (rs_variant 5). CTAs [0, C) push,
+// CTAs [C, 2C) fold: pusher b stores sub-slice t of every chunk q into
+// member q's staging slot [gi] and publishes unit t+1 to q in the READY
+// words of CTA index b; folder C+b waits for unit t+1 from every peer's
+// pusher b and folds sub-slice t from local memory, so the fold of t runs
+// while the pushes of t+1.. are in flight (NVLink and HBM busy at once) and
+// the data travels as posted writes (all-to-all: 668-682 GB/s vs 628-637 for
+// peer loads, profiles/r1_engine_probe_p4.md). Entry: every pusher b
+// announces "my staging is free" to the peers' pushers b. No exit barrier:
+// folders read only local memory.
+template <int DT, bool VEC, int ORDER, int MAXP>
+__global__ void __launch_bounds__(kThreads) k_rs_direct_pp(const __grid_constant__ LaunchParams P) {
+  using R = RUnit<DT, VEC>;
+  using T = typename R::T;
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  const int gs = c.gs, gi = c.gi, C = P.ctas / 2, nsub = P.nsub > 1 ? P.nsub : 4;
+  const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
+  const bool pusher = c.b < C;
+  const int b = pusher ? c.b : c.b - C;
+  if (b >= C) return;  // odd grid: the spare CTA has no slice
+  int64_t lo, hi;
+  split32(P.blk, C, b, lo, hi);
+  const T *own = reinterpret_cast<const T *>(P.send[c.r]) + P.base[c.y];
+  if (pusher) {
+    cta_signal_entry(c, peers);  // my staging is free
+    if (!cta_wait_mask(c, peers, 0, true)) return;
+    for (int t = 0; t < nsub; ++t) {
+      int64_t a, e;
+      split32(hi - lo, nsub, t, a, e);
+      for (int i = 1; i < gs; ++i) {
+        const int q = (gi + i) % gs;
+        copy_typed<T>(reinterpret_cast<T *>(P.recv[c.world(q)]) + (int64_t)gi * P.blk, own + (int64_t)q * P.istride,
+                      lo + a, lo + e);
+      }
+      cta_signal_mask(c, peers, t + 1);  // sub-slice t of my chunks has landed
+    }
+    return;
+  }
+  const T *src[MAXP];
+#pragma unroll
+  for (int i = 0; i < MAXP; ++i) {
+    int q;
+    if (ORDER == O_RING) q = (gi + 1 + i) % gs;
+    else if (ORDER == O_REC) q = gi ^ i;
+    else q = i;
+    if (i >= gs) q = gi;
+    src[i] = (q == gi) ? own + (int64_t)gi * P.istride : reinterpret_cast<const T *>(P.recv[c.r]) + (int64_t)q * P.blk;
+  }
+  T *dst = reinterpret_cast<T *>(P.out[c.r]);
+  for (int t = 0; t < nsub; ++t) {
+    if (!cta_wait_mask(c, peers, t + 1, false, b)) return;
+    int64_t a, e;
+    split32(hi - lo, nsub, t, a, e);
+    rs_fold<DT, VEC, ORDER, MAXP>(src, gs, 0, dst, lo + a, lo + e);
+  }
+}
 
 // ============================================================================
 // LL direct collectives (small messages; protocol in device.cuh)

@@ -181,6 +181,25 @@ KernelFn ag_kernel(int algo, int U) {
   return nullptr;
 }
 
+template <int DT, bool VEC>
+KernelFn rs_direct_pp_kernel(int order, int maxp) {
+#define RSP(O)                                                          \
+  if (order == O) {                                                     \
+    if (!VEC) return (KernelFn)k_rs_direct_pp<DT, VEC, O, 16>;          \
+    switch (maxp) {                                                     \
+      case 2: return (KernelFn)k_rs_direct_pp<DT, VEC, O, 2>;           \
+      case 4: return (KernelFn)k_rs_direct_pp<DT, VEC, O, 4>;           \
+      case 8: return (KernelFn)k_rs_direct_pp<DT, VEC, O, 8>;           \
+      default: return (KernelFn)k_rs_direct_pp<DT, VEC, O, 16>;         \
+    }                                                                   \
+  }
+  RSP(O_RING)
+  RSP(O_REC)
+  RSP(O_RANK)
+#undef RSP
+  return nullptr;
+}
+
 template <int DT, bool VEC, bool PUSH>
 KernelFn rs_direct_kernel(int order, int maxp) {
 #define RSD(O)                                                          \
@@ -204,6 +223,7 @@ template <int DT, bool VEC>
 KernelFn rs_kernel_dt(int algo, int order, int maxp, int variant) {
   if (algo == A_RING) return variant == 1 ? (KernelFn)k_rs_ring_push<DT, VEC> : (KernelFn)k_rs_ring<DT, VEC>;
   if (algo == A_REC) return variant == 1 ? (KernelFn)k_rs_rec_push<DT, VEC> : (KernelFn)k_rs_rec<DT, VEC>;
+  if (variant == 5) return rs_direct_pp_kernel<DT, VEC>(order, maxp);
   return variant == 1 ? rs_direct_kernel<DT, VEC, true>(order, maxp) : rs_direct_kernel<DT, VEC, false>(order, maxp);
 }
 
@@ -420,6 +440,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     }
   }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
+  if (pl.coll == PCCL_REDUCE_SCATTER && pl.variant == 5) ctas = std::max(2, ctas & ~1);  // pusher / folder pairs
   {
     // every CTA must be co-resident (they wait on each other); the occupancy
     // query costs microseconds of host time, so it is cached per configuration
@@ -921,7 +942,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
       const bool send_reg = resolve(w, ranks[0], sends[0], gs * chunk_bytes, &seg, &off);
       v = (!send_reg || algo == A_RING) ? 1 : 0;
     }
-    pl.variant = v == 1 ? 1 : 0;
+    pl.variant = v == 1 ? 1 : (v == 5 && algo == A_DIRECT) ? 5 : 0;
   }
   Binder B{w, stream};
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -931,7 +952,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     if (!member) return PCCL_ERR_INDEX_OUT_OF_RANGE;
     pl.rows.push_back({r, c});
     B.cursor = 0;
-    if (pl.variant == 1) {
+    if (pl.variant == 1 || pl.variant == 5) {
       // push: send is read locally only; peers write into my staging (recv)
       pl.send[r] = (char *)sends[i];
       if (!B.scratch(r, gs * chunk_bytes, pl.recv)) return B.status;
@@ -1496,7 +1517,7 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
-  if (is_variant && value > (strcmp(key, "ag_variant") ? 4 : 5)) return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5 copy engine (AG)
+  if (is_variant && value > 5) return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct)
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;

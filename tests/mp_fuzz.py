@@ -100,6 +100,7 @@ def main() -> int:
         kind = rng.choice(["sym", "plain", "misaligned", "host"] if coll != "hier" else ["sym", "plain", "misaligned"])
         w.set_param("item_kib", rng.choice([0, 0, 16, 64]))  # direct kernels: static slices / work items
         w.set_param("ag_variant", rng.choice([-1, -1, 5] if ce else [-1]))  # 5: copy engine (ring / recursive)
+        w.set_param("rs_variant", rng.choice([-1, -1, 5]))  # 5: pipelined push (direct only; others fall back)
         total_in = n if coll == "ag" else n * p
         total_out = n * p if coll == "ag" else n
         if kind == "sym":
@@ -153,6 +154,7 @@ def main() -> int:
     for it in range(a.iters):
         if it % 25 == 24:
             w.set_param("ag_variant", -1)
+            w.set_param("rs_variant", -1)
             w.set_param("item_kib", 0)
             # CUDA graph: capture three fixed calls on a side stream, replay, verify
             side = torch.cuda.Stream(dev)

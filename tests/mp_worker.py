@@ -103,6 +103,21 @@ def main() -> int:
             check(f"ce_ag_inplace_n{n}", out.cpu().numpy(), want)
         w.set_param("ag_variant", -1)
     sync_point("copy_engine")
+    # direct RS, pipelined push (rs_variant 5) in every fold order, fp32 + bf16
+    comm.world.set_param("rs_variant", 5)
+    for n in (37, 4096, 300_000):
+        rs_in = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+        for order in ["ring", "rank"] + (["recursive"] if pow2 else []):
+            want = oracle.direct_reduce_scatter(rs_in, "f32", order)[rank]
+            got = pkg.direct_reduce_scatter(comm, torch.from_numpy(rs_in[rank]).cuda(), order=order)
+            check(f"rs_pp_{order}_n{n}", got.cpu().numpy(), want)
+        bf = [oracle.f32_to_bf16(x) for x in rs_in]
+        xb = torch.from_numpy(bf[rank].view(np.int16)).view(torch.bfloat16).cuda()
+        got = pkg.direct_reduce_scatter(comm, xb, order="ring")
+        check(f"rs_pp_bf16_n{n}", got.view(torch.int16).cpu().numpy().view(np.uint16),
+              oracle.direct_reduce_scatter(bf, "bf16", "ring")[rank])
+    comm.world.set_param("rs_variant", -1)
+    sync_point("rs_pipelined_push")
     # NVLS multicast segment (switch-executed AG stores / RS loads)
     from paper_2504_18658_b200 import nvls as NV
 

@@ -314,6 +314,43 @@ def test_direct_dynamic_work_items_bit_exact(p, item_kib):
             assert _bits_equal(got, want_ag if i % 2 == 0 else want_rs[r]), (r, i)
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 8, 16])
+@pytest.mark.parametrize("order", ["ring", "recursive", "rank"])
+def test_direct_pipelined_push_bit_exact(p, order):
+    """rs_variant 5 (pusher / folder CTAs, sub-slice pipelined): fp32 in every
+    fold order and bf16 give the oracle's bits; odd and even grids."""
+    if order == "recursive" and p & (p - 1):
+        pytest.skip("recursive order needs a power of two")
+    pkg = _pkg()
+    n = 100_003 if p < 16 else 20_011
+    rng = np.random.default_rng(p * 7 + len(order))
+    ins = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    ins_bf = [oracle.f32_to_bf16(x) for x in ins]
+    want = oracle.direct_reduce_scatter(ins, "f32", order)
+    want_bf = oracle.direct_reduce_scatter(ins_bf, "bf16", order)
+
+    def body(c):
+        w = c.world
+        w.set_param("rs_variant", 5)
+        try:
+            out = []
+            for ctas in (0, 7):  # auto (even) and an odd grid (spare CTA)
+                w.set_param("ctas", ctas)
+                out.append(pkg.direct_reduce_scatter(c, torch.from_numpy(ins[c.rank]).cuda(), order=order).cpu().numpy())
+                xb = torch.from_numpy(ins_bf[c.rank].view(np.int16)).view(torch.bfloat16).cuda()
+                yb = pkg.direct_reduce_scatter(c, xb, order=order)
+                out.append(yb.view(torch.int16).cpu().numpy().view(np.uint16))
+        finally:
+            w.set_param("rs_variant", -1)
+            w.set_param("ctas", 0)
+        return out
+
+    outs = pkg.run_ranks(p, body)
+    for r in range(p):
+        for i, got in enumerate(outs[r]):
+            assert _bits_equal(got, (want if i % 2 == 0 else want_bf)[r]), (r, i)
+
+
 def test_back_to_back_calls_reuse_buffers():
     """Epoch flags never reset: many consecutive calls stay correct."""
     pkg = _pkg()

@@ -62,9 +62,11 @@ def main():
             for v in map(int, args.variants.split(",")):
                 if v in (2, 3, 4) and algo != "direct":
                     continue
-                if v >= 2 and kind == "rs":
+                if v in (2, 3) and kind == "rs":
                     continue
-                if v == 5 and algo == "direct":  # copy engine: ring / recursive doubling all-gather
+                if v == 5 and kind == "ag" and algo == "direct":  # AG 5: copy engine (ring / recursive doubling)
+                    continue
+                if v == 5 and kind == "rs" and algo != "direct":  # RS 5: pipelined push (direct)
                     continue
                 for tm in (args.tma.split(",") if v >= 2 else ["0x0"]):
                     combos.append((v, *map(int, tm.split("x"))))
