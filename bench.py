@@ -734,8 +734,16 @@ def main():
         args.no_extra = args.no_cpu = True
     if args.impl == "reference":
         run_reference(args)
-    else:
+        return
+    try:
         run_gpu(args)
+    except Exception as exc:  # a failed run still leaves one parseable line (rank 0)
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s",
+                              "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+                              "warmup": args.warmup, "higher_is_better": True,
+                              "error": f"{type(exc).__name__}: {exc}"[:400]}), flush=True)
+        raise
 
 
 if __name__ == "__main__":
