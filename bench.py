@@ -219,9 +219,12 @@ def run_gpu(args):
     # more ranks than GPUs (a functional check of the N-rank path on a smaller
     # box: ranks time-share GPUs, bootstrap over gloo, no NCCL / NVLS extras;
     # the numbers are not performance numbers)
-    shared = real and world_size > torch.cuda.device_count()
-    if shared:
-        local_rank %= torch.cuda.device_count()
+    ndev = torch.cuda.device_count()
+    # (a launcher that hands each rank its own GPU through CUDA_VISIBLE_DEVICES
+    # shows one device per process: that is not sharing)
+    shared = real and world_size > ndev and not os.environ.get("CUDA_VISIBLE_DEVICES")
+    if local_rank >= ndev:
+        local_rank %= ndev
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     red_dev = torch.device("cpu") if shared else dev  # where max-over-ranks reductions live
