@@ -221,8 +221,8 @@ def run_gpu(args):
     # the numbers are not performance numbers)
     ndev = torch.cuda.device_count()
     # (a launcher that hands each rank its own GPU through CUDA_VISIBLE_DEVICES
-    # shows one device per process: that is not sharing)
-    shared = real and world_size > ndev and not os.environ.get("CUDA_VISIBLE_DEVICES")
+    # shows exactly one device per process: that is not sharing)
+    shared = real and world_size > ndev > 1
     if local_rank >= ndev:
         local_rank %= ndev
     torch.cuda.set_device(local_rank)
