@@ -37,14 +37,12 @@ def main() -> int:
     ap.add_argument("--seed", type=int, default=0)
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    shared = os.environ.get("PCCL_TEST_SHARED_GPUS") == "1"  # more ranks than GPUs (see mp_worker.py)
     local = int(os.environ.get("LOCAL_RANK", rank))
-    dev = torch.device("cuda", local % torch.cuda.device_count() if shared else local)
+    if local >= torch.cuda.device_count():  # one process per GPU, never shared
+        raise SystemExit(f"rank {rank}: local rank {local} >= {torch.cuda.device_count()} visible GPUs")
+    dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    if shared:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("nccl", device_id=dev)
     import paper_2504_18658_b200 as pkg
 
     from paper_2504_18658_b200 import _lib, collectives as C
@@ -55,7 +53,7 @@ def main() -> int:
     C.PIPE_MIN_BYTES, C.PIPE_SLICE_BYTES = 64 << 10, 16 << 10  # host buffers: sliced path, many slices
     from paper_2504_18658_b200 import nvls as NV
 
-    seg = NV.create_nvls_segment(w, 64 << 20) if not shared and NV.nvls_supported(w) else None
+    seg = NV.create_nvls_segment(w, 64 << 20) if NV.nvls_supported(w) else None
     rng = random.Random(a.seed)  # same stream on every rank: SPMD calls
     pow2 = p & (p - 1) == 0
     grids = [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]

@@ -20,16 +20,13 @@ import oracle  # noqa: E402
 def main() -> int:
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    # PCCL_TEST_SHARED_GPUS=1: more ranks than GPUs (ranks time-share a GPU,
-    # bootstrap over gloo since NCCL refuses two ranks on one device) — a slow
-    # but complete check of the p = 8 host logic on a 4-GPU box
-    shared = os.environ.get("PCCL_TEST_SHARED_GPUS") == "1"
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local % torch.cuda.device_count() if shared else local)
-    if shared:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    # one process per GPU, never more ranks than devices (ranks spinning on
+    # each other's flags from one GPU can deadlock the device)
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: local rank {local} >= {torch.cuda.device_count()} visible GPUs")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2504_18658_b200 as pkg
 
     comm = pkg.init_from_torch()
@@ -121,7 +118,7 @@ def main() -> int:
     # NVLS multicast segment (switch-executed AG stores / RS loads)
     from paper_2504_18658_b200 import nvls as NV
 
-    if not shared and NV.nvls_supported(comm.world):  # one multicast member per device
+    if NV.nvls_supported(comm.world):  # one multicast member per device
         seg = NV.create_nvls_segment(comm.world, 16 << 20)
         try:
             for n in (8, 4096, 300_000):

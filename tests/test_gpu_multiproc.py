@@ -64,20 +64,3 @@ def test_real_mode_fuzz(nproc):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("FUZZ OK") == nproc, out[-4000:]
-
-
-def test_real_mode_parity_more_ranks_than_gpus():
-    """Twice as many ranks as GPUs (ranks time-share a GPU, gloo bootstrap):
-    on a 4-GPU box this runs the full real-mode parity worker at p = 8, the
-    driver's largest scaling point, including the hierarchical 2x4 / 4x2
-    groupings. Slow (every handshake may wait for a time slice), functional only."""
-    if _ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
-    nproc = min(8, 2 * _ngpus())
-    env = dict(os.environ, PCCL_TIMEOUT_MS="120000", PCCL_TEST_SHARED_GPUS="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr=127.0.0.1", "--master-port=29540", os.path.join(ROOT, "tests", "mp_worker.py")]
-    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0, out[-4000:]
-    assert out.count("OK") >= nproc, out[-4000:]
