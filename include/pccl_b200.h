@@ -19,11 +19,13 @@
  * (collkit/transport/base.py:131-134), which is what keeps the per-group epoch
  * counters (the replacement for next_base_tag) in agreement without any
  * host-side coordination. Epochs live in device memory, so every collective
- * is CUDA-graph capturable (segments must be sized before capture). All calls
- * on one member set must be ordered on the device (one stream, or streams
- * ordered with events): two concurrent collectives on the same group share its
- * epoch word and corrupt each other, exactly like two unordered NCCL calls on
- * one communicator.
+ * is CUDA-graph capturable (segments must be sized before capture). All
+ * collectives on one WORLD must be ordered on the device (one stream, or
+ * streams ordered with events), including calls on different sub-groups: the
+ * staging segment and the per-rank-pair LL channels are world resources, and
+ * two concurrent collectives on the same group share its epoch word, exactly
+ * like two unordered NCCL calls on one communicator. Independent streams of
+ * collectives need independent worlds.
  */
 #ifndef PCCL_B200_H
 #define PCCL_B200_H
@@ -119,6 +121,10 @@ int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
  * << 16 | kind << 12 | unit; kind 1 start, 2 wait done, 3 signal, 4 end),
  * 128 words per CTA, laid out [row][cta][event]; copies the last launch's. */
 int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas);
+/* Param "trace" = K (2..8): the last K launches are kept; back = 0 is the
+ * latest. Events: (t_ns << 16 | kind << 12 | unit), kinds 1 start, 2 wait
+ * done, 3 signal, 4 exit-barrier done, 5 CTA exit. Diagnostics only. */
+int pccl_world_trace_at(pccl_world_t w, int back, uint64_t *host, size_t cap_words, int *rows, int *ctas);
 
 /* ---- symmetric segments ---------------------------------------------- */
 int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id);

@@ -39,6 +39,8 @@ _SIGS = {
     "pccl_world_set_timeout_ms": (_i, [_vp, ctypes.c_int64]),
     "pccl_world_set_param": (_i, [_vp, ctypes.c_char_p, ctypes.c_int64]),
     "pccl_world_trace": (_i, [_vp, ctypes.POINTER(ctypes.c_uint64), _sz, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
+    "pccl_world_trace_at": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_uint64), _sz, ctypes.POINTER(_i),
+                                 ctypes.POINTER(_i)]),
     "pccl_world_get_param": (_i, [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]),
     "pccl_segment_create": (_i, [_vp, _sz, ctypes.POINTER(_i)]),
     "pccl_segment_export": (_i, [_vp, _i, _vp]),

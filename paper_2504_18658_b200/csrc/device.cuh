@@ -94,7 +94,8 @@ struct LaunchParams {
 };
 
 #define PCCL_TRACE_EVENTS 128
-enum TraceKind { TR_START = 1, TR_WAIT = 2, TR_SIGNAL = 3, TR_END = 4 };
+#define PCCL_TRACE_LAUNCHES 8
+enum TraceKind { TR_START = 1, TR_WAIT = 2, TR_SIGNAL = 3, TR_END = 4, TR_EXIT = 5, TR_RESIDENT = 6 };
 
 // --------------------------------------------------------------------------
 // memory-model primitives
@@ -146,6 +147,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
+  const uint64_t t_resident = P.trace ? global_timer_ns() : 0;  // CTA scheduled (before the PDL wait)
   pdl_wait();
   pdl_launch_dependents();
   Ctx c;
@@ -164,16 +166,21 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
   c.ntr = 0;
   c.ll_peers = 0;
-  if (c.tr && threadIdx.x == 0) c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
+  if (c.tr && threadIdx.x == 0) {
+    c.tr[c.ntr++] = (t_resident << 16) | (TR_RESIDENT << 12);
+    c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
+  }
   return c;
 }
 
 // Runs when a kernel returns (any path): the last CTA of the row to leave
 // publishes the epoch for the next launch on this stream.
 struct CtaEpilogue {
-  const Ctx &c;
-  __device__ explicit CtaEpilogue(const Ctx &cc) : c(cc) {}
+  Ctx &c;
+  __device__ explicit CtaEpilogue(Ctx &cc) : c(cc) {}
   __device__ ~CtaEpilogue() {
+    if (c.tr && threadIdx.x == 0 && c.ntr < PCCL_TRACE_EVENTS)
+      c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)TR_EXIT << 12);
     if (threadIdx.x == 0) {
       unsigned long long *ctrl = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF);
       const unsigned long long old = atomicAdd(ctrl + 1, 1ull);
@@ -277,8 +284,7 @@ __device__ __forceinline__ int spin_ready(const Ctx &c, const uint64_t *w, int u
 
 // CTA-wide: wait until member m has completed `unit` (its call signature is
 // verified on every wait). Returns false (after aborting the group) on error.
-__device__ __forceinline__ bool cta_wait(Ctx &c, int m, int unit, bool check_meta = true) {
-  (void)check_meta;
+__device__ __forceinline__ bool cta_wait(Ctx &c, int m, int unit) {
   int code = 0;
   if (threadIdx.x == 0) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, c.b), unit);
   int ok = __syncthreads_and(code == 0);
@@ -295,8 +301,7 @@ __device__ __forceinline__ bool cta_wait(Ctx &c, int m, int unit, bool check_met
 
 // CTA-wide: wait for every member in `mask` (bit m) to complete `unit`.
 // `idx`: the writers' CTA index whose words to wait on (default: mine).
-__device__ __forceinline__ bool cta_wait_mask(Ctx &c, uint32_t mask, int unit, bool check_meta = true, int idx = -1) {
-  (void)check_meta;
+__device__ __forceinline__ bool cta_wait_mask(Ctx &c, uint32_t mask, int unit, int idx = -1) {
   int code = 0;
   const int m = threadIdx.x;
   if (m < c.gs && ((mask >> m) & 1u)) code = spin_ready(c, Ctx::word(c.my_slot, F_READY, m, idx < 0 ? c.b : idx), unit);
@@ -350,8 +355,6 @@ __device__ __forceinline__ void cta_signal_entry(Ctx &c, uint32_t mask, int unit
   if (m < c.gs && ((mask >> m) & 1u)) st_relaxed_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
   trace_ev(c, TR_SIGNAL, unit);
 }
-// Kept for call-site symmetry: the signature now travels in the READY word.
-__device__ __forceinline__ void cta_publish_meta(const Ctx &, uint32_t) {}
 
 // Exit barrier: tell every member in `to` that this CTA has finished reading
 // their buffers; wait until every member in `from` has finished reading ours.

@@ -52,12 +52,11 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
   Ctx c = make_ctx(P);
   CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
-  cta_publish_meta(c, peers);
   cta_signal_entry(c, peers);  // my send buffer is ready
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   if (P.item > 0) {
     // items (range j, sub-block t, source i), source fastest so that the
     // CTAs in flight spread over all peers
@@ -88,7 +87,6 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ La
   CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
-  cta_publish_meta(c, 1u << next);
   // step 0: own block into recv (the block the ring starts forwarding)
   for (int t = 0; t < nsub; ++t) {
     int64_t lo, hi;
@@ -101,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring(const __grid_constant__ La
   for (int s = 1; s < gs; ++s) {
     const int blk = (c.gi - s + gs) % gs;  // block received at reference step s-1
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, prev, (s - 1) * nsub + t, s == 1 && t == 0)) return;
+      if (!cta_wait(c, prev, (s - 1) * nsub + t)) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j)
@@ -120,7 +118,6 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
-  cta_publish_meta(c, partners);
   for (int t = 0; t < nsub; ++t) {
     int64_t lo, hi;
     cta_subslice(c, t, lo, hi);
@@ -133,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
     const char *pr = P.recv[c.world(partner)];
     const int start = (partner >> k) << k, width = 1 << k;
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, partner, k * nsub + t, t == 0)) return;
+      if (!cta_wait(c, partner, k * nsub + t)) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int i = start; i < start + width; ++i)
@@ -175,11 +172,10 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   Ctx c = make_ctx(P);
   CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
-  cta_publish_meta(c, peers);
   cta_signal_entry(c, peers);  // my recv may be written
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   if (P.item > 0) {
     // items (range j, sub-block t, destination i), destination fastest
     const int nd = c.gs - 1;
@@ -202,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   }
   cta_signal_mask(c, peers, 1);  // my block (this CTA's items of it) has landed in your recv
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
-  if (!cta_wait_mask(c, peers, 1, false)) return;
+  if (!cta_wait_mask(c, peers, 1)) return;
 }
 
 struct TmaCfg {
@@ -231,11 +227,10 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_tma(const __grid_constan
   CtaEpilogue fin(c);
   const uint32_t peers = ((1u << c.gs) - 1) & ~(1u << c.gi);
   TmaRing R = tma_ring_setup(dsm, P.tma_stages, P.tma_tile);
-  cta_publish_meta(c, peers);
   cta_signal_mask(c, peers, 0);
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   if (threadIdx.x == 0) {
     fence_proxy_async();
     const int gs = c.gs, nsb = P.nsubblk;
@@ -259,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_tma(const __grid_constan
   }
   if (PUSH) {
     cta_signal_mask(c, peers, 1);
-    if (!cta_wait_mask(c, peers, 1, false)) return;
+    if (!cta_wait_mask(c, peers, 1)) return;
   } else {
     cta_exit(c, peers, peers);
   }
@@ -283,7 +278,6 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ La
   CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
-  cta_publish_meta(c, 1u << next);
   cta_signal_entry(c, 1u << next, nsub - 1);  // my send is ready (units 0..nsub-1)
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
   const int pw = c.world(prev);
@@ -292,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring(const __grid_constant__ La
     const bool last = (s == gs - 1);
     const char *remote = (s == 1) ? P.send[pw] : P.work[pw];
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, prev, (s - 1) * nsub + t, s == 1 && t == 0)) return;
+      if (!cta_wait(c, prev, (s - 1) * nsub + t)) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j) {
@@ -314,7 +308,6 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
-  cta_publish_meta(c, partners);
   cta_signal_entry(c, 1u << rechalf_partner(c.gi, gs, 0), nsub - 1);  // my send is ready (units 0..nsub-1)
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
   int lo_c = 0, hi_c = gs;
@@ -328,7 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
     const char *remote = (k == 0) ? P.send[pw] : P.work[pw];
     const char *local = (k == 0) ? sendp : workp;
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, partner, k * nsub + t, t == 0)) return;
+      if (!cta_wait(c, partner, k * nsub + t)) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int ch = m0; ch < m1; ++ch)
@@ -365,15 +358,14 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
   CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
-  cta_publish_meta(c, (1u << next) | (1u << prev));
   cta_signal_entry(c, 1u << prev);  // my recv is free
-  if (!cta_wait(c, next, 0, true)) return;
+  if (!cta_wait(c, next, 0)) return;
   char *my = P.recv[c.r];
   char *nx = P.recv[c.world(next)];
   for (int s = 0; s < gs - 1; ++s) {
     const int blk = (c.gi - s + gs) % gs;
     for (int t = 0; t < nsub; ++t) {
-      if (s > 0 && !cta_wait(c, prev, push_unit(s - 1, nsub, t), s == 1 && t == 0)) return;
+      if (s > 0 && !cta_wait(c, prev, push_unit(s - 1, nsub, t))) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j) {
@@ -386,7 +378,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
     }
   }
   for (int t = 0; t < nsub; ++t)
-    if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t), gs == 2 && t == 0)) return;
+    if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t))) return;
   if (P.local_copy) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
@@ -402,16 +394,15 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << recdbl_partner(c.gi, k);
-  cta_publish_meta(c, partners);
   cta_signal_entry(c, partners);  // my recv is free
   char *my = P.recv[c.r];
   for (int k = 0; k < L; ++k) {
     const int partner = recdbl_partner(c.gi, k);
-    if (!cta_wait(c, partner, 0, true)) return;
+    if (!cta_wait(c, partner, 0)) return;
     char *pr = P.recv[c.world(partner)];
     const int start = (c.gi >> k) << k, width = 1 << k;
     for (int t = 0; t < nsub; ++t) {
-      if (k > 0 && !cta_wait(c, recdbl_partner(c.gi, k - 1), push_unit(k - 1, nsub, t), false)) return;
+      if (k > 0 && !cta_wait(c, recdbl_partner(c.gi, k - 1), push_unit(k - 1, nsub, t))) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int i = start; i < start + width; ++i)
@@ -424,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
     }
   }
   for (int t = 0; t < nsub; ++t)
-    if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t), false)) return;
+    if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t))) return;
   if (P.local_copy) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
@@ -441,9 +432,8 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring_push(const __grid_constant
   CtaEpilogue fin(c);
   const int gs = c.gs, nsub = P.nsub;
   const int prev = ring_prev(c.gi, gs), next = ring_next(c.gi, gs);
-  cta_publish_meta(c, (1u << next) | (1u << prev));
   cta_signal_entry(c, 1u << prev);  // my staging is free
-  if (!cta_wait(c, next, 0, true)) return;
+  if (!cta_wait(c, next, 0)) return;
   char *sendp = P.send[c.r], *stg = P.recv[c.r], *nstg = P.recv[c.world(next)], *outp = P.out[c.r];
   {
     const int ch = (c.gi - 1 + gs) % gs;  // initial carry (collectives.py:98)
@@ -459,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_ring_push(const __grid_constant
     const int ch = ((c.gi - s - 1) % gs + gs) % gs;
     const bool last = (s == gs - 1);
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, prev, push_unit(s - 1, nsub, t), s == 1 && t == 0)) return;
+      if (!cta_wait(c, prev, push_unit(s - 1, nsub, t))) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j) {
@@ -483,7 +473,6 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant_
   const int gs = c.gs, nsub = P.nsub, L = ilog2(gs);
   uint32_t partners = 0;
   for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
-  cta_publish_meta(c, partners);
   cta_signal_entry(c, partners);  // my staging is free
   char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r], *stgp = P.recv[c.r];
   // staging slot of absolute chunk ch received at step k (region base = gs - gs/2^k chunks)
@@ -494,7 +483,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant_
   // step "-1": raw input over theirs_0 into partner_0's staging region 0
   {
     const int partner = rechalf_partner(c.gi, gs, 0);
-    if (!cta_wait(c, partner, 0, true)) return;
+    if (!cta_wait(c, partner, 0)) return;
     const int half = gs / 2, mid = half;
     const int t0 = c.gi < mid ? mid : 0, t1 = c.gi < mid ? gs : mid;  // theirs_0
     char *pst = P.recv[c.world(partner)];
@@ -521,13 +510,13 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec_push(const __grid_constant_
       const int h2 = (m1 - m0) / 2, mid2 = m0 + h2;
       if (c.gi < mid2) { n0 = m0; n1 = mid2; } else { n0 = mid2; n1 = m1; }
       nxt = c.gi ^ h2;
-      if (!cta_wait(c, nxt, 0, false)) return;
+      if (!cta_wait(c, nxt, 0)) return;
       nst = P.recv[c.world(nxt)];
     }
     const int t_lo = (n0 == m0) ? n1 : m0;  // theirs_{k+1} = mine_k \ mine_{k+1}
     const char *local = (k == 0) ? sendp : workp;
     for (int t = 0; t < nsub; ++t) {
-      if (!cta_wait(c, partner, push_unit(k, nsub, t), false)) return;
+      if (!cta_wait(c, partner, push_unit(k, nsub, t))) return;
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int ch = m0; ch < m1; ++ch)
@@ -629,9 +618,8 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   CtaEpilogue fin(c);
   const int gs = c.gs, gi = c.gi;
   const uint32_t peers = ((1u << gs) - 1) & ~(1u << gi);
-  cta_publish_meta(c, peers);
   cta_signal_entry(c, peers);  // pull: my send is ready; push: my staging is free
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   const T *own = reinterpret_cast<const T *>(P.send[c.r]);
@@ -645,7 +633,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
       copy_typed<T>(dst, own + P.base[c.y] + (int64_t)q * P.istride, lo, hi);
     }
     cta_signal_mask(c, peers, 1);  // my chunks have landed
-    if (!cta_wait_mask(c, peers, 1, false)) return;
+    if (!cta_wait_mask(c, peers, 1)) return;
   }
   const T *src[MAXP];
 #pragma unroll
@@ -705,7 +693,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_pp(const __grid_constant
   const T *own = reinterpret_cast<const T *>(P.send[c.r]) + P.base[c.y];
   if (pusher) {
     cta_signal_entry(c, peers);  // my staging is free
-    if (!cta_wait_mask(c, peers, 0, true)) return;
+    if (!cta_wait_mask(c, peers, 0)) return;
     for (int t = 0; t < nsub; ++t) {
       int64_t a, e;
       split32(hi - lo, nsub, t, a, e);
@@ -730,7 +718,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_pp(const __grid_constant
   }
   T *dst = reinterpret_cast<T *>(P.out[c.r]);
   for (int t = 0; t < nsub; ++t) {
-    if (!cta_wait_mask(c, peers, t + 1, false, b)) return;
+    if (!cta_wait_mask(c, peers, t + 1, b)) return;
     int64_t a, e;
     split32(hi - lo, nsub, t, a, e);
     rs_fold<DT, VEC, ORDER, MAXP>(src, gs, 0, dst, lo + a, lo + e);
@@ -970,7 +958,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls_ag(const __grid_constant__ La
   cta_signal_entry(c, peers);
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   fence_proxy_alias();
   const uint4 *src = reinterpret_cast<const uint4 *>(P.send[c.r]);
   uint4 *mc = reinterpret_cast<uint4 *>(P.recv[c.r]) + P.base[c.y] + (int64_t)c.gi * P.istride;
@@ -988,7 +976,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls_ag(const __grid_constant__ La
   // plus the system-scope release of the "landed" flags publishes them
   fence_proxy_alias();
   cta_signal_mask(c, peers, 1);
-  if (!cta_wait_mask(c, peers, 1, false)) return;
+  if (!cta_wait_mask(c, peers, 1)) return;
   fence_proxy_alias();
 }
 
@@ -1003,7 +991,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls_rs(const __grid_constant__ La
   cta_signal_entry(c, peers);
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
-  if (!cta_wait_mask(c, peers, 0, true)) return;
+  if (!cta_wait_mask(c, peers, 0)) return;
   fence_proxy_alias();
   const uint4 *mc = reinterpret_cast<const uint4 *>(P.send[c.r]) + P.base[c.y] + (int64_t)c.gi * P.istride;
   uint4 *dst = reinterpret_cast<uint4 *>(P.out[c.r]);
@@ -1131,6 +1119,52 @@ __global__ void __launch_bounds__(kThreads) k_reduce_inplace(char *acc, const ch
     typename R::Acc s = R::load(a[i]);
     acc_add<typename R::Acc, R::N>(s, R::load(__ldg(b + i)));
     a[i] = R::store(s);
+  }
+}
+
+// ============================================================================
+// Copy-engine all-gather handshake (ag_variant 5). One thread spins on a META
+// word of my arena until it reaches `target`, bounded by the world timeout;
+// on timeout or abort it records the error and floods ABORT into every
+// member's META words of the group's slot, so no peer's wait is left spinning
+// (a stream memory-op wait has no deadline, which is why this is a kernel).
+// ============================================================================
+struct CeWait {
+  const uint64_t *word;
+  uint64_t target;
+  volatile int *err;
+  int64_t timeout_ns;
+  int gs;
+  uint64_t *meta[PCCL_MAXR];  // per member: META rows of the slot in its arena
+};
+
+__global__ void k_ce_wait(const __grid_constant__ CeWait W) {
+  __shared__ int s_code;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = global_timer_ns();
+    int code = 0;
+    uint32_t it = 0;
+    while (true) {
+      const uint64_t v = ld_acquire_sys(W.word);
+      if (v & PCCL_ABORT_BIT) { code = (int)(v & 0xff); break; }
+      if (v >= W.target) break;
+      if ((++it & 255u) == 0) {
+        if (*W.err != 0) { code = *W.err; break; }
+        if (global_timer_ns() - t0 > (uint64_t)W.timeout_ns) { code = 5; break; }  // PCCL_ERR_TIMEOUT
+      }
+    }
+    if (code && *W.err == 0) {
+      *W.err = code;
+      __threadfence_system();
+    }
+    s_code = code;
+  }
+  __syncthreads();
+  if (s_code) {
+    const uint64_t v = PCCL_ABORT_BIT | (uint64_t)s_code;
+    for (int m = 0; m < W.gs; ++m)
+      for (int i = threadIdx.x; i < PCCL_MAXR * PCCL_MAX_CTAS; i += blockDim.x) st_relaxed_sys(W.meta[m] + i, v);
+    __threadfence_system();
   }
 }
 

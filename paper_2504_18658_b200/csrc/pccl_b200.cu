@@ -76,6 +76,7 @@ struct pccl_world {
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
+  int64_t trace_seq = 0;  // launches traced since tracing was (re)enabled
   uint32_t meta_skew[PCCL_MAXR] = {};
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
   std::map<OccKey, int> occ_cache;              // co-resident CTAs per SM, per (kernel, threads, smem)
@@ -462,12 +463,22 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   }
   P.ctas = ctas;
   if (w->p_trace) {
+    // trace = K: the last K launches, one buffer each (K = 1: memset before
+    // every launch; K > 1: consecutive launches run back to back, the ring is
+    // cleared once when tracing starts)
+    const int K = (int)std::min<int64_t>(w->p_trace, PCCL_TRACE_LAUNCHES);
     const size_t words = (size_t)PCCL_MAXR * PCCL_MAX_CTAS * PCCL_TRACE_EVENTS;
-    if (!w->trace_buf) CK(cudaMalloc((void **)&w->trace_buf, words * 8));
-    CK(cudaMemsetAsync(w->trace_buf, 0, (size_t)nrows * ctas * PCCL_TRACE_EVENTS * 8, stream));
-    P.trace = w->trace_buf;
+    if (!w->trace_buf) CK(cudaMalloc((void **)&w->trace_buf, words * 8 * PCCL_TRACE_LAUNCHES));
+    if (K == 1 || w->trace_seq == 0 || w->trace_rows != nrows || w->trace_ctas != ctas) {
+      CK(cudaMemsetAsync(w->trace_buf, 0, words * 8 * (size_t)K, stream));
+      w->trace_seq = 0;
+    }
+    P.trace = w->trace_buf + words * (size_t)(w->trace_seq % K);
+    w->trace_seq++;
     w->trace_rows = nrows;
     w->trace_ctas = ctas;
+  } else {
+    w->trace_seq = 0;
   }
   dim3 grid(ctas, nrows), block(threads);
   if (w->emu) {
@@ -647,28 +658,52 @@ CUdeviceptr ce_flag(const pccl_comm *c, int q, int src, int idx) {
   return (CUdeviceptr)(slot + ((size_t)(F_META * PCCL_MAXR + src) * PCCL_MAX_CTAS + idx));
 }
 
-// Returns -1 when the copy-engine path does not apply (caller uses kernels).
+// The path is explicitly requested (ag_variant 5) and must be taken by every
+// member: a call that does not qualify on this rank fails with Unsupported
+// instead of silently falling back to kernels (a member that took the other
+// path would wait for this one until the timeout, not forever: the waits are
+// k_ce_wait kernels bounded by the world timeout, which flood ABORT on expiry).
 int ce_all_gather(pccl_comm *c, int algo, const void *send, void *recv, size_t blk, cudaStream_t s) {
   pccl_world *w = c->w;
-  if (w->emu || algo == A_DIRECT || blk == 0) return -1;
+  if (w->emu) return PCCL_ERR_UNSUPPORTED;
+  if (blk == 0) return PCCL_SUCCESS;
   MemOps &mo = memops(w->device);
-  if (!mo.ok) return -1;
+  if (!mo.ok) return PCCL_ERR_UNSUPPORTED;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
-    return -1;
+    return PCCL_ERR_UNSUPPORTED;
   }
   const int gs = c->gs, gi = c->gi, me = w->rank;
   int seg;
   size_t off;
-  if (gi < 0 || !resolve(w, me, recv, gs * blk, &seg, &off)) return -1;  // peers write into my recv
+  if (gi < 0 || !resolve(w, me, recv, gs * blk, &seg, &off)) return PCCL_ERR_UNSUPPORTED;  // peers write into my recv
   auto peer_recv = [&](int m) { return w->segs[seg].ptr[c->members[m]] + off; };
   char *my = (char *)recv;
   const uint64_t e = ++w->ce_calls[c->slot];
   CUstream cs = (CUstream)s;
+  CeWait W;
+  memset(&W, 0, sizeof(W));
+  W.target = e;
+  W.err = w->err_dev;
+  W.timeout_ns = w->p_timeout_ms * 1000000ll;
+  W.gs = gs;
+  for (int m = 0; m < gs; ++m)
+    W.meta[m] = (uint64_t *)c->w->segs[0].ptr[c->members[m]] + (size_t)c->slot * PCCL_SLOT_WORDS +
+                (size_t)F_META * PCCL_MAXR * PCCL_MAX_CTAS;
+  auto wait = [&](int src, int idx) -> int {
+    W.word = (const uint64_t *)ce_flag(c, me, src, idx);
+    k_ce_wait<<<1, 128, 0, s>>>(W);
+    return cuda_err(cudaGetLastError());
+  };
 #define CE(x)                                        \
   do {                                               \
     if ((x) != CUDA_SUCCESS) return PCCL_ERR_CUDA;   \
+  } while (0)
+#define CW(x)                \
+  do {                       \
+    const int st_ = (x);     \
+    if (st_) return st_;     \
   } while (0)
   if ((const char *)send != my + (size_t)gi * blk)
     CK(cudaMemcpyAsync(my + (size_t)gi * blk, send, blk, cudaMemcpyDeviceToDevice, s));
@@ -678,26 +713,27 @@ int ce_all_gather(pccl_comm *c, int algo, const void *send, void *recv, size_t b
       CE(mo.write64(cs, ce_flag(c, c->members[gi ^ (1 << k)], gi, 0), e, 0));
     for (int k = 0; k < L; ++k) {
       const int partner = gi ^ (1 << k), start = (gi >> k) << k;
-      CE(mo.wait64(cs, ce_flag(c, me, partner, 0), e, CU_STREAM_WAIT_VALUE_GEQ));
-      if (k > 0) CE(mo.wait64(cs, ce_flag(c, me, gi ^ (1 << (k - 1)), k), e, CU_STREAM_WAIT_VALUE_GEQ));
+      CW(wait(partner, 0));
+      if (k > 0) CW(wait(gi ^ (1 << (k - 1)), k));
       CK(cudaMemcpyAsync(peer_recv(partner) + (size_t)start * blk, my + (size_t)start * blk, ((size_t)1 << k) * blk,
                          cudaMemcpyDeviceToDevice, s));
       CE(mo.write64(cs, ce_flag(c, c->members[partner], gi, k + 1), e, 0));
     }
-    CE(mo.wait64(cs, ce_flag(c, me, gi ^ (1 << (L - 1)), L), e, CU_STREAM_WAIT_VALUE_GEQ));
+    CW(wait(gi ^ (1 << (L - 1)), L));
   } else {  // ring: step t forwards block (gi - t + 1) to next (collectives.py:70-75)
     const int next = (gi + 1) % gs, prev = (gi + gs - 1) % gs;
     CE(mo.write64(cs, ce_flag(c, c->members[prev], gi, 0), e, 0));
-    CE(mo.wait64(cs, ce_flag(c, me, next, 0), e, CU_STREAM_WAIT_VALUE_GEQ));
+    CW(wait(next, 0));
     for (int t = 1; t < gs; ++t) {
-      if (t > 1) CE(mo.wait64(cs, ce_flag(c, me, prev, t - 1), e, CU_STREAM_WAIT_VALUE_GEQ));
+      if (t > 1) CW(wait(prev, t - 1));
       const int b = (gi - t + 1 + gs) % gs;
       CK(cudaMemcpyAsync(peer_recv(next) + (size_t)b * blk, my + (size_t)b * blk, blk, cudaMemcpyDeviceToDevice, s));
       CE(mo.write64(cs, ce_flag(c, c->members[next], gi, t), e, 0));
     }
-    CE(mo.wait64(cs, ce_flag(c, me, prev, gs - 1), e, CU_STREAM_WAIT_VALUE_GEQ));
+    CW(wait(prev, gs - 1));
   }
 #undef CE
+#undef CW
   return PCCL_SUCCESS;
 }
 
@@ -800,6 +836,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.send_sub_stride = (int64_t)count;
   if (algo == A_DIRECT && use_ll(w, w->p_ag_variant, blk_bytes, gs)) {
     pl.variant = 4;
+    pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
     Binder B{w, stream};
     std::vector<std::pair<char *, char *>> copy_out;
     for (size_t i = 0; i < ranks.size(); ++i) {
@@ -817,17 +854,14 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
       if (!ll_local(B, r, snd, blk_bytes, true, nullptr)) return B.status;
       pl.send[r] = snd;
       pl.recv[r] = rcv;
-      pl.local_copy = snd != rcv + (size_t)gi * blk_bytes;
+      pl.local_copy |= snd != rcv + (size_t)gi * blk_bytes;  // any row (a self-copy is harmless)
     }
     int s = launch(w, pl, stream);
     if (s) return s;
     for (auto &co : copy_out) CK(cudaMemcpyAsync(co.second, co.first, gs * blk_bytes, cudaMemcpyDeviceToDevice, stream));
     return PCCL_SUCCESS;
   }
-  if (w->p_ag_variant == 5 && ranks.size() == 1) {
-    const int st = ce_all_gather(c, algo, sends[0], recvs[0], blk_bytes, stream);
-    if (st >= 0) return st;
-  }
+  if (w->p_ag_variant == 5 && !w->emu && algo != A_DIRECT) return ce_all_gather(c, algo, sends[0], recvs[0], blk_bytes, stream);
   {
     // Data movement. auto: push (posted NVLink stores, saturates the links
     // with few SMs) whenever the output is symmetric; a direct all-gather into
@@ -845,6 +879,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   }
   Binder B{w, stream};
   std::vector<std::pair<char *, char *>> copy_out;  // (staged recv, user recv)
+  pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
   for (size_t i = 0; i < ranks.size(); ++i) {
     const int r = ranks[i];
     int gi = -1;
@@ -859,19 +894,19 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
       if (!B.symmetric(r, recvs[i], gs * blk_bytes, false, pl.recv, &staged)) return B.status;
       if (staged) copy_out.push_back({staged, (char *)recvs[i]});
       pl.send[r] = (char *)sends[i];
-      pl.local_copy = staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+      pl.local_copy |= staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
     } else if (algo == A_DIRECT) {
       // peers read my send; my recv is written locally only
       if (!B.symmetric(r, sends[i], blk_bytes, true, pl.send, nullptr)) return B.status;
       pl.recv[r] = (char *)recvs[i];
-      pl.local_copy = sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+      pl.local_copy |= sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
     } else {
       // peers forward out of my recv; send is read locally only
       char *staged = nullptr;
       if (!B.symmetric(r, recvs[i], gs * blk_bytes, false, pl.recv, &staged)) return B.status;
       if (staged) copy_out.push_back({staged, (char *)recvs[i]});
       pl.send[r] = (char *)sends[i];
-      pl.local_copy = staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
+      pl.local_copy |= staged || sends[i] != (const char *)recvs[i] + (size_t)gi * blk_bytes;
     }
   }
   pl.place = w->emu ? 0 : B.place;
@@ -910,6 +945,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.out_sub_stride = (int64_t)recvcount;
   if (algo == A_DIRECT && use_ll(w, w->p_rs_variant, chunk_bytes, gs)) {
     pl.variant = 4;
+    pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
     Binder B{w, stream};
     std::vector<std::pair<char *, char *>> copy_out;
     for (size_t i = 0; i < ranks.size(); ++i) {
@@ -1330,6 +1366,9 @@ int pccl_nvls_all_gather(pccl_comm_t c, int id, const void *send, size_t out_off
   pl.send[me] = (char *)send;
   pl.recv[me] = (char *)w->nvls[id].mc_va + out_offset;
   pl.out[me] = (char *)w->nvls[id].uc_va + out_offset;
+  // segment and offset enter the call signature: ranks that pass different
+  // offsets get LengthMismatch instead of multicasting to different places
+  pl.place = (uint32_t)id * 7919u + (uint32_t)(out_offset >> 4) + 1u;
   return launch(w, pl, (cudaStream_t)stream);
 }
 
@@ -1354,6 +1393,7 @@ int pccl_nvls_reduce_scatter(pccl_comm_t c, int id, size_t in_offset, void *recv
   pl.rows.push_back({me, c});
   pl.send[me] = (char *)w->nvls[id].mc_va + in_offset;
   pl.out[me] = (char *)recv;
+  pl.place = (uint32_t)id * 7919u + (uint32_t)(in_offset >> 4) + 1u;
   return launch(w, pl, (cudaStream_t)stream);
 }
 #undef CUD
@@ -1533,17 +1573,25 @@ int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value) {
   return PCCL_SUCCESS;
 }
 
-int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas) {
-  if (!w || !host || !rows || !ctas) return PCCL_ERR_INVALID_ARGUMENT;
+int pccl_world_trace_at(pccl_world_t w, int back, uint64_t *host, size_t cap_words, int *rows, int *ctas) {
+  if (!w || !host || !rows || !ctas || back < 0) return PCCL_ERR_INVALID_ARGUMENT;
   *rows = w->trace_rows;
   *ctas = w->trace_ctas;
-  if (!w->trace_buf) return PCCL_SUCCESS;
+  if (!w->trace_buf || w->trace_seq == 0) return PCCL_SUCCESS;
+  const int K = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_trace, PCCL_TRACE_LAUNCHES));
+  if (back >= K || back >= w->trace_seq) return PCCL_ERR_INVALID_ARGUMENT;
+  const size_t stride = (size_t)PCCL_MAXR * PCCL_MAX_CTAS * PCCL_TRACE_EVENTS;
   const size_t words = (size_t)w->trace_rows * w->trace_ctas * PCCL_TRACE_EVENTS;
   if (cap_words < words) return PCCL_ERR_OUT_OF_MEMORY;
+  const int64_t idx = ((w->trace_seq - 1 - back) % K + K) % K;
   CK(cudaSetDevice(w->device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(host, w->trace_buf, words * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(host, w->trace_buf + stride * (size_t)idx, words * 8, cudaMemcpyDeviceToHost));
   return PCCL_SUCCESS;
+}
+
+int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas) {
+  return pccl_world_trace_at(w, 0, host, cap_words, rows, ctas);
 }
 
 int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id) {

@@ -188,14 +188,16 @@ class World:
         check(lib().pccl_world_get_param(self.handle, key.encode(), ctypes.byref(v)), f"get_param({key})")
         return v.value
 
-    def trace(self):
-        """Events of the last launch (param "trace" = 1): list over rows of
-        lists over CTAs of (t_ns, kind, unit) tuples; kinds: 1 start, 2 wait
-        done, 3 signal, 4 end."""
+    def trace(self, back: int = 0):
+        """Events of a traced launch (param "trace" = K keeps the last K;
+        back = 0 is the latest): list over rows of lists over CTAs of
+        (t_ns, kind, unit) tuples; kinds: 1 start, 2 wait done, 3 signal,
+        4 exit barrier done, 5 CTA exit."""
         cap = 16 * 320 * 128
         buf = (ctypes.c_uint64 * cap)()
         rows, ctas = ctypes.c_int(), ctypes.c_int()
-        check(lib().pccl_world_trace(self.handle, buf, cap, ctypes.byref(rows), ctypes.byref(ctas)), "trace")
+        check(lib().pccl_world_trace_at(self.handle, back, buf, cap, ctypes.byref(rows), ctypes.byref(ctas)),
+              "trace")
         out = []
         for y in range(rows.value):
             row = []

@@ -98,6 +98,15 @@ def main() -> int:
             out[rank * n:(rank + 1) * n].copy_(x)
             pkg.all_gather_into_tensor(out, out[rank * n:(rank + 1) * n], comm, algorithm="ring")
             check(f"ce_ag_inplace_n{n}", out.cpu().numpy(), want)
+        # an output the peers cannot write into does not qualify: every rank
+        # gets Unsupported (no silent per-rank fallback, no launch)
+        w.set_param("ag_variant", 5)
+        try:
+            pkg.all_gather_into_tensor(torch.empty(4096 * p, device=x.device), torch.zeros(4096, device=x.device),
+                                       comm, algorithm="ring")
+            failures.append("ce_ag_unregistered_accepted")
+        except pkg.errors.Unsupported:
+            pass
         w.set_param("ag_variant", -1)
     sync_point("copy_engine")
     # direct RS, pipelined push (rs_variant 5) in every fold order, fp32 + bf16
