@@ -274,7 +274,7 @@ def seeded_fill(t: torch.Tensor, seed: int) -> None:
 # the rig: real ranks (one process per GPU) or p ranks emulated on one GPU
 # ---------------------------------------------------------------------------
 class Rig:
-    def __init__(self, real: bool, p: int, rank: int, dev: torch.device, dist=None):
+    def __init__(self, real: bool, p: int, rank: int, dev: torch.device, dist=None, comm=None):
         import paper_2504_18658_b200 as pkg
         from paper_2504_18658_b200 import _lib
         from paper_2504_18658_b200.communicator import _emu_group, emulated_world
@@ -283,7 +283,7 @@ class Rig:
         self.real, self.p, self.rank, self.dev, self.dist = real, p, rank, dev, dist
         self.stream = torch.cuda.current_stream(dev)
         if real:
-            self.comm = pkg.init_from_torch(device=dev.index)
+            self.comm = comm if comm is not None else pkg.init_from_torch(device=dev.index)
             self.world = self.comm.world
             self.ghandle = self.comm.handle
         else:

@@ -278,6 +278,67 @@ def main() -> int:
     if not torch.equal(gout, want[rank * 4096:(rank + 1) * 4096]) or not torch.equal(gag, want):
         failures.append("cuda_graph")
 
+    # BASELINE configs at FULL size over real NVLink: every
+    # rank regenerates its peers' seeded inputs on its own GPU and checks its
+    # whole output bit for bit against the reduction-order restatement
+    # (bench.expected_rs, pinned against the oracle by tests/test_bench.py)
+    if os.environ.get("PCCL_TEST_FULLSIZE", "1") == "1":
+        import bench
+
+        rig = bench.Rig(True, p, rank, torch.device("cuda", torch.cuda.current_device()), dist, comm=comm)
+        MiB = 1 << 20
+        # C1: all-gather fp32, 64 MiB output, ring
+        n = 64 * MiB // 4 // p
+        bi, bo = rig.sym(n, torch.float32), rig.sym(n * p, torch.float32)
+        sd = rig.new_seed()
+        rig.fill(bi, sd)
+        rig.ag("ring", bi, bo, n, 0)()
+        if not rig.verify_ag(bi, bo, sd, n, torch.float32):
+            failures.append("full_c1_ag_f32_64MiB_ring")
+        # C2: reduce-scatter bf16, 128 MiB input, recursive halving (+ direct)
+        n = 128 * MiB // 2 // p
+        bi, bo = rig.sym(n * p, torch.bfloat16), rig.sym(n, torch.bfloat16)
+        sd = rig.new_seed()
+        rig.fill(bi, sd)
+        for algo in (["recursive"] if pow2 else []) + ["direct", "ring"]:
+            order = "recursive" if algo == "recursive" else "ring"
+            rig.rs(algo, order, bi, bo, n, 1)()
+            if not rig.verify_rs(bi, bo, sd, n, torch.bfloat16, algo, order):
+                failures.append(f"full_c2_rs_bf16_128MiB_{algo}")
+        # C3: hierarchical AG + RS fp32, 256 MiB, every virtual grouping
+        n = 256 * MiB // 4 // p
+        ai, ao = rig.sym(n, torch.float32), rig.sym(n * p, torch.float32)
+        ri, ro = rig.sym(n * p, torch.float32), rig.sym(n, torch.float32)
+        sa, sr = rig.new_seed(), rig.new_seed()
+        rig.fill(ai, sa)
+        rig.fill(ri, sr)
+        for N in [g for g in (2, 4) if p % g == 0 and 1 < g < p]:
+            for inter in ["ring"] + (["recursive"] if N & (N - 1) == 0 else []):
+                rig.hier("ag", N, p // N, inter, ai, ao, n, 0)()
+                if not rig.verify_ag(ai, ao, sa, n, torch.float32):
+                    failures.append(f"full_c3_hier_ag_{N}x{p // N}_{inter}")
+                rig.hier("rs", N, p // N, inter, ri, ro, n, 0)()
+                if not rig.verify_rs(ri, ro, sr, n, torch.float32, "hierarchical", grid=(N, p // N), inter=inter):
+                    failures.append(f"full_c3_hier_rs_{N}x{p // N}_{inter}")
+        del ai, ao, ri, ro, bi, bo
+        # C5: GPT-3-style 7B per-layer shapes, bf16, direct AG + RS
+        n7 = bench.P7 // p
+        prm, full = rig.sym(n7, torch.bfloat16), rig.sym(n7 * p, torch.bfloat16)
+        sd = rig.new_seed()
+        rig.fill(prm, sd)
+        rig.ag("direct", prm, full, n7, 1)()
+        if not rig.verify_ag(prm, full, sd, n7, torch.bfloat16):
+            failures.append("full_c5_ag_bf16_direct")
+        del prm, full
+        grad, gsh = rig.sym(n7 * p, torch.bfloat16), rig.sym(n7, torch.bfloat16)
+        sd = rig.new_seed()
+        rig.fill(grad, sd)
+        rig.rs("direct", "ring", grad, gsh, n7, 1)()
+        if not rig.verify_rs(grad, gsh, sd, n7, torch.bfloat16, "direct", "ring"):
+            failures.append("full_c5_rs_bf16_direct")
+        del grad, gsh
+        sync_point("fullsize")
+
     # online calibration: every rank must resolve "auto" identically afterwards
     from paper_2504_18658_b200 import selector, tuning
 
