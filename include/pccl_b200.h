@@ -167,6 +167,12 @@ int pccl_hier_all_gather(pccl_world_t w, int N, int M, int inter_algo, const voi
                          int dtype, void *stream);
 int pccl_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter_algo, const void *send, void *recv,
                              size_t recvcount, int dtype, void *stream);
+/* The same over any communicator of N x M members (hierarchy.py:129-134:
+ * only the size must match the topology); topology rank g = member g. */
+int pccl_hier_all_gather_comm(pccl_comm_t c, int N, int M, int inter_algo, const void *send, void *recv,
+                              size_t count, int dtype, void *stream);
+int pccl_hier_reduce_scatter_comm(pccl_comm_t c, int N, int M, int inter_algo, const void *send, void *recv,
+                                  size_t recvcount, int dtype, void *stream);
 
 /* ---- emulation-mode variants: per-member pointer arrays, one launch ----- */
 int pccl_emu_all_gather(pccl_comm_t c, int algo, const void *const *sends, void *const *recvs, size_t count,
@@ -177,6 +183,10 @@ int pccl_emu_hier_all_gather(pccl_world_t w, int N, int M, int inter_algo, const
                              void *const *recvs, size_t count, int dtype, void *stream);
 int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter_algo, const void *const *sends,
                                  void *const *recvs, size_t recvcount, int dtype, void *stream);
+int pccl_emu_hier_all_gather_comm(pccl_comm_t c, int N, int M, int inter_algo, const void *const *sends,
+                                  void *const *recvs, size_t count, int dtype, void *stream);
+int pccl_emu_hier_reduce_scatter_comm(pccl_comm_t c, int N, int M, int inter_algo, const void *const *sends,
+                                      void *const *recvs, size_t recvcount, int dtype, void *stream);
 /* Test hook: perturb one member's call signature so the device-side
  * cross-rank check must raise LengthMismatch (tests/test_collectives.py:172-175). */
 int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask);

@@ -62,6 +62,11 @@ _SIGS = {
     "pccl_emu_reduce_scatter": (_i, [_vp, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _vp]),
     "pccl_emu_hier_all_gather": (_i, [_vp, _i, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _vp]),
     "pccl_emu_hier_reduce_scatter": (_i, [_vp, _i, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _vp]),
+    "pccl_hier_all_gather_comm": (_i, [_vp, _i, _i, _i, _vp, _vp, _sz, _i, _vp]),
+    "pccl_hier_reduce_scatter_comm": (_i, [_vp, _i, _i, _i, _vp, _vp, _sz, _i, _vp]),
+    "pccl_emu_hier_all_gather_comm": (_i, [_vp, _i, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _vp]),
+    "pccl_emu_hier_reduce_scatter_comm": (_i, [_vp, _i, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i,
+                                               _vp]),
     "pccl_emu_debug_meta_skew": (_i, [_vp, _i, ctypes.c_uint32]),
     "pccl_probe": (_i, [_vp, _i, _i, ctypes.c_uint32, _sz, _i, _vp]),
     "pccl_shuffle": (_i, [_i, _vp, _vp, _i, _i, _sz, _i, _vp]),

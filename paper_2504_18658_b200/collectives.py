@@ -22,6 +22,7 @@ pass ``out=`` a tensor from ``comm.world.empty`` to skip every staging copy.
 from __future__ import annotations
 
 import enum
+import math
 import os
 
 import numpy as np
@@ -480,12 +481,32 @@ def direct_reduce_scatter(comm, buf, *, order: str = "ring", out=None):
     return _run(comm, buf, True, "direct", order, out)
 
 
+def _resolve_auto(comm, collective: str, m_bytes: int) -> str:
+    """``auto``: the measured winner for (collective, p, size). Real mode
+    first calibrates the live world when the table has nothing within 8x of
+    this size at this GPU count (``tuning.autotune``, SPMD-uniform: the table
+    and the call are the same on every rank, so every rank measures the same
+    candidates and agrees on the result). Emulated ranks (no NVLink to
+    measure) and calls under CUDA-graph capture use the table as it is, with
+    the one-shot ``direct`` when it has nothing for this p."""
+    from . import selector, tuning
+
+    p = comm.size
+    if p > 1 and not comm.emulated and not torch.cuda.is_current_stream_capturing():
+        t = selector.flat_table()
+        have = [e.m_bytes for e in (t.entries if t else []) if e.collective == collective and e.p == p]
+        # calibration size: this size's power-of-two bucket, clamped to 1-256 MiB
+        m = 1 << max(20, min(28, (max(m_bytes, 1) - 1).bit_length()))
+        m = max(16 * p * 4, m // (16 * p * 4) * (16 * p * 4))  # whole 16-byte units per rank, any dtype
+        if not have or min(abs(math.log2(m / h)) for h in have) > 3:
+            tuning.autotune(comm, collective, m, dtype=torch.float32 if collective == "all_gather" else torch.bfloat16)
+    return selector.choose_algorithm(collective, p, m_bytes)
+
+
 def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
     """Dispatching all-gather; ``auto`` picks from the measured selector."""
     if algorithm == "auto":
-        from .selector import choose_algorithm
-
-        algorithm = choose_algorithm("all_gather", comm.size, _nbytes(buf) * comm.size)
+        algorithm = _resolve_auto(comm, "all_gather", _nbytes(buf) * comm.size)
     if algorithm not in ALL_GATHER_ALGOS:
         raise Unsupported(f"unknown all-gather algorithm {algorithm!r}")
     return _run(comm, buf, False, algorithm, "ring", out)
@@ -494,9 +515,7 @@ def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
 def reduce_scatter(comm, buf, *, algorithm: str = "auto", order: str = "ring", out=None):
     """Dispatching reduce-scatter; ``auto`` picks from the measured selector."""
     if algorithm == "auto":
-        from .selector import choose_algorithm
-
-        algorithm = choose_algorithm("reduce_scatter", comm.size, _nbytes(buf))
+        algorithm = _resolve_auto(comm, "reduce_scatter", _nbytes(buf))
     if algorithm not in REDUCE_SCATTER_ALGOS:
         raise Unsupported(f"unknown reduce-scatter algorithm {algorithm!r}")
     return _run(comm, buf, True, algorithm, order, out)

@@ -1027,11 +1027,29 @@ pccl_comm *cached_group(pccl_world *w, const std::vector<int> &members, int comm
 }
 
 // --------------------------------------------------------------------------
-// hierarchical (hierarchy.py:158-195); virtual nodes n = g / M, local j = g % M
+// hierarchical (hierarchy.py:158-195) over a communicator `mem` (topology rank
+// g -> world rank mem[g]; the world communicator is mem = 0..p-1); virtual
+// nodes n = g / M, local j = g % M
 // --------------------------------------------------------------------------
-int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector<int> &ranks,
+bool topo_index(const pccl_world *w, const std::vector<int> &mem, int *topo) {
+  for (int q = 0; q < PCCL_MAXR; ++q) topo[q] = -1;
+  for (size_t g = 0; g < mem.size(); ++g) {
+    if (mem[g] < 0 || mem[g] >= w->nranks || topo[mem[g]] >= 0) return false;
+    topo[mem[g]] = (int)g;
+  }
+  return true;
+}
+std::vector<int> iota_ranks(int n) {
+  std::vector<int> v(n);
+  for (int i = 0; i < n; ++i) v[i] = i;
+  return v;
+}
+
+int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M, int inter, const std::vector<int> &ranks,
                        const void *const *sends, void *const *recvs, size_t count, int dtype, cudaStream_t stream) {
-  if (N < 1 || M < 1 || N * M != w->nranks) return PCCL_ERR_LENGTH_MISMATCH;
+  if (N < 1 || M < 1 || N * M != (int)mem.size()) return PCCL_ERR_LENGTH_MISMATCH;
+  int topo[PCCL_MAXR];  // world rank -> topology rank g (index in mem)
+  if (!topo_index(w, mem, topo)) return PCCL_ERR_INVALID_ARGUMENT;
   if (inter != A_RING && inter != A_REC) return PCCL_ERR_INVALID_ARGUMENT;
   if (inter == A_REC && !is_pow2(N)) return PCCL_ERR_NON_POWER_OF_TWO;
   const size_t es = dt_size(dtype);
@@ -1061,22 +1079,22 @@ int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector
     pl.place = place;
     pl.variant = w->p_ag_variant == 0 ? 0 : 1;  // push (recv is symmetric)
     for (size_t i = 0; i < ranks.size(); ++i) {
-      const int r = ranks[i], j = r % M;
-      std::vector<int> mem;
-      for (int n = 0; n < N; ++n) mem.push_back(n * M + j);
-      pccl_comm *g = cached_group(w, mem, 1 + j);
+      const int r = ranks[i], j = topo[r] % M;
+      std::vector<int> grp;
+      for (int n = 0; n < N; ++n) grp.push_back(mem[n * M + j]);
+      pccl_comm *g = cached_group(w, grp, 1 + j);
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
       pl.base[r] = (int64_t)j * count;
       pl.send[r] = (char *)sends[i];
     }
-    for (int q = 0; q < w->nranks; ++q) { pl.recv[q] = outp[q]; pl.base[q] = (int64_t)(q % M) * count; }
+    for (int g = 0; g < N * M; ++g) { const int q = mem[g]; pl.recv[q] = outp[q]; pl.base[q] = (int64_t)(g % M) * count; }
     int s = launch(w, pl, stream);
     if (s) return s;
   } else {
     for (size_t i = 0; i < ranks.size(); ++i) {
       const int r = ranks[i];
-      if (count) CK(cudaMemcpyAsync(outp[r] + (size_t)r * count * es, sends[i], count * es, cudaMemcpyDeviceToDevice, stream));
+      if (count) CK(cudaMemcpyAsync(outp[r] + (size_t)topo[r] * count * es, sends[i], count * es, cudaMemcpyDeviceToDevice, stream));
     }
   }
   // phase 2: intra-node ring all-gather; member l's block = N sub-blocks at
@@ -1088,14 +1106,14 @@ int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector
     pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
     pl.variant = w->p_ag_variant == 0 ? 0 : 1;
     for (size_t i = 0; i < ranks.size(); ++i) {
-      const int r = ranks[i], n = r / M;
-      std::vector<int> mem;
-      for (int l = 0; l < M; ++l) mem.push_back(n * M + l);
-      pccl_comm *g = cached_group(w, mem, 1 + M + n);
+      const int r = ranks[i], n = topo[r] / M;
+      std::vector<int> grp;
+      for (int l = 0; l < M; ++l) grp.push_back(mem[n * M + l]);
+      pccl_comm *g = cached_group(w, grp, 1 + M + n);
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
     }
-    for (int q = 0; q < w->nranks; ++q) { pl.recv[q] = outp[q]; pl.send[q] = outp[q]; }
+    for (int g = 0; g < N * M; ++g) { const int q = mem[g]; pl.recv[q] = outp[q]; pl.send[q] = outp[q]; }
     int s = launch(w, pl, stream);
     if (s) return s;
   }
@@ -1103,9 +1121,11 @@ int do_hier_all_gather(pccl_world *w, int N, int M, int inter, const std::vector
   return PCCL_SUCCESS;
 }
 
-int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::vector<int> &ranks,
+int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, int M, int inter, const std::vector<int> &ranks,
                            const void *const *sends, void *const *recvs, size_t n, int dtype, cudaStream_t stream) {
-  if (N < 1 || M < 1 || N * M != w->nranks) return PCCL_ERR_LENGTH_MISMATCH;
+  if (N < 1 || M < 1 || N * M != (int)mem.size()) return PCCL_ERR_LENGTH_MISMATCH;
+  int topo[PCCL_MAXR];  // world rank -> topology rank g (index in mem)
+  if (!topo_index(w, mem, topo)) return PCCL_ERR_INVALID_ARGUMENT;
   if (inter != A_RING && inter != A_REC) return PCCL_ERR_INVALID_ARGUMENT;
   if (inter == A_REC && !is_pow2(N)) return PCCL_ERR_NON_POWER_OF_TWO;
   if (dtype != PCCL_FLOAT32 && dtype != PCCL_BFLOAT16 && dtype != PCCL_FLOAT16) return PCCL_ERR_UNSUPPORTED;
@@ -1131,15 +1151,15 @@ int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::ve
     pl.nsubblk = N; pl.blk = (int64_t)n; pl.sub_stride = (int64_t)M * n; pl.istride = (int64_t)n;
     pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
-      const int r = ranks[i], nd = r / M;
-      std::vector<int> mem;
-      for (int l = 0; l < M; ++l) mem.push_back(nd * M + l);
-      pccl_comm *g = cached_group(w, mem, 1 + M + nd);
+      const int r = ranks[i], nd = topo[r] / M;
+      std::vector<int> grp;
+      for (int l = 0; l < M; ++l) grp.push_back(mem[nd * M + l]);
+      pccl_comm *g = cached_group(w, grp, 1 + M + nd);
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
     }
     pl.variant = w->p_rs_variant == 1 ? 1 : 0;  // pull by default (measured faster here); push: staging = work
-    for (int q = 0; q < w->nranks; ++q) {
+    for (int q : mem) {
       pl.send[q] = sendp[q];
       pl.work[q] = work[q];
       pl.recv[q] = work[q];
@@ -1159,16 +1179,16 @@ int do_hier_reduce_scatter(pccl_world *w, int N, int M, int inter, const std::ve
     pl.coll = PCCL_REDUCE_SCATTER; pl.algo = inter; pl.dtype = dtype; pl.count = n; pl.gs = N;
     pl.blk = (int64_t)n; pl.istride = (int64_t)n; pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
-      const int r = ranks[i], j = r % M;
-      std::vector<int> mem;
-      for (int nd = 0; nd < N; ++nd) mem.push_back(nd * M + j);
-      pccl_comm *g = cached_group(w, mem, 1 + j);
+      const int r = ranks[i], j = topo[r] % M;
+      std::vector<int> grp;
+      for (int nd = 0; nd < N; ++nd) grp.push_back(mem[nd * M + j]);
+      pccl_comm *g = cached_group(w, grp, 1 + j);
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
       pl.out[r] = (char *)recvs[i];
     }
     pl.variant = w->p_rs_variant == 1 ? 1 : 0;
-    for (int q = 0; q < w->nranks; ++q) {
+    for (int q : mem) {
       pl.send[q] = part[q];
       pl.work[q] = work2[q];
       pl.recv[q] = work2[q];
@@ -1774,7 +1794,8 @@ int pccl_hier_all_gather(pccl_world_t w, int N, int M, int inter, const void *se
   if (e) return e;
   const void *s[1] = {send};
   void *r[1] = {recv};
-  return do_hier_all_gather(w, N, M, inter, one(w->rank), s, r, count, dtype, (cudaStream_t)stream);
+  return do_hier_all_gather(w, iota_ranks(w->nranks), N, M, inter, one(w->rank), s, r, count, dtype,
+                            (cudaStream_t)stream);
 }
 
 int pccl_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const void *send, void *recv, size_t recvcount,
@@ -1784,7 +1805,8 @@ int pccl_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const void
   if (e) return e;
   const void *s[1] = {send};
   void *r[1] = {recv};
-  return do_hier_reduce_scatter(w, N, M, inter, one(w->rank), s, r, recvcount, dtype, (cudaStream_t)stream);
+  return do_hier_reduce_scatter(w, iota_ranks(w->nranks), N, M, inter, one(w->rank), s, r, recvcount, dtype,
+                                (cudaStream_t)stream);
 }
 
 int pccl_emu_all_gather(pccl_comm_t c, int algo, const void *const *sends, void *const *recvs, size_t count, int dtype,
@@ -1806,7 +1828,7 @@ int pccl_emu_hier_all_gather(pccl_world_t w, int N, int M, int inter, const void
   if (!w || !w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
   std::vector<int> ranks;
   for (int r = 0; r < w->nranks; ++r) ranks.push_back(r);
-  return do_hier_all_gather(w, N, M, inter, ranks, sends, recvs, count, dtype, (cudaStream_t)stream);
+  return do_hier_all_gather(w, ranks, N, M, inter, ranks, sends, recvs, count, dtype, (cudaStream_t)stream);
 }
 
 int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const void *const *sends, void *const *recvs,
@@ -1814,7 +1836,45 @@ int pccl_emu_hier_reduce_scatter(pccl_world_t w, int N, int M, int inter, const 
   if (!w || !w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
   std::vector<int> ranks;
   for (int r = 0; r < w->nranks; ++r) ranks.push_back(r);
-  return do_hier_reduce_scatter(w, N, M, inter, ranks, sends, recvs, recvcount, dtype, (cudaStream_t)stream);
+  return do_hier_reduce_scatter(w, ranks, N, M, inter, ranks, sends, recvs, recvcount, dtype, (cudaStream_t)stream);
+}
+
+// Over any communicator of N*M members (hierarchy.py:129-134 only requires
+// the communicator size to match the topology): topology rank g is member g.
+int pccl_hier_all_gather_comm(pccl_comm_t c, int N, int M, int inter, const void *send, void *recv, size_t count,
+                              int dtype, void *stream) {
+  if (!c || c->w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(c->w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_hier_all_gather(c->w, std::vector<int>(c->members, c->members + c->gs), N, M, inter, one(c->w->rank), s, r,
+                            count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_hier_reduce_scatter_comm(pccl_comm_t c, int N, int M, int inter, const void *send, void *recv,
+                                  size_t recvcount, int dtype, void *stream) {
+  if (!c || c->w->emu) return PCCL_ERR_INVALID_ARGUMENT;
+  int e = check_world_err(c->w);
+  if (e) return e;
+  const void *s[1] = {send};
+  void *r[1] = {recv};
+  return do_hier_reduce_scatter(c->w, std::vector<int>(c->members, c->members + c->gs), N, M, inter, one(c->w->rank),
+                                s, r, recvcount, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_hier_all_gather_comm(pccl_comm_t c, int N, int M, int inter, const void *const *sends,
+                                  void *const *recvs, size_t count, int dtype, void *stream) {
+  if (!c || !c->w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> mem(c->members, c->members + c->gs);
+  return do_hier_all_gather(c->w, mem, N, M, inter, mem, sends, recvs, count, dtype, (cudaStream_t)stream);
+}
+
+int pccl_emu_hier_reduce_scatter_comm(pccl_comm_t c, int N, int M, int inter, const void *const *sends,
+                                      void *const *recvs, size_t recvcount, int dtype, void *stream) {
+  if (!c || !c->w->emu || !sends || !recvs) return PCCL_ERR_INVALID_ARGUMENT;
+  std::vector<int> mem(c->members, c->members + c->gs);
+  return do_hier_reduce_scatter(c->w, mem, N, M, inter, mem, sends, recvs, recvcount, dtype, (cudaStream_t)stream);
 }
 
 int pccl_emu_debug_meta_skew(pccl_world_t w, int rank, uint32_t xor_mask) {

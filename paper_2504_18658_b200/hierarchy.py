@@ -30,7 +30,7 @@ from .collectives import (
     as_elements,
     is_power_of_two,
 )
-from .errors import LengthMismatch, NonPowerOfTwo, NotDivisible, Unsupported
+from .errors import LengthMismatch, NonPowerOfTwo, NotDivisible
 from .selector import CalibrationTable, CostParams, choose_inter_algorithm
 from .topology import Topology
 from .world import TORCH_DTYPES
@@ -135,11 +135,11 @@ def shuffle_global_to_local_major(buf, num_nodes: int, gpus_per_node: int, block
 # hierarchical collectives
 # ---------------------------------------------------------------------------
 def _check_world(plan: HierPlan, comm):
+    """hierarchy.py:129-134: the communicator's size must match the topology
+    (any communicator: topology rank g is its member g)."""
     topo = plan.topo
     if comm.size != topo.world_size:
         raise LengthMismatch(f"communicator size {comm.size} != topology world {topo.world_size}")
-    if comm.members != tuple(range(comm.world.nranks)):
-        raise Unsupported("hierarchical collectives run on the world communicator")
 
 
 def _hier(plan: HierPlan, comm, buf, reduce: bool, out=None):
@@ -188,12 +188,12 @@ def _hier(plan: HierPlan, comm, buf, reduce: bool, out=None):
                      torch.empty(out_numel, dtype=sends[0].dtype, device=comm.device) for a in args]
         stream = _stream(comm.device)
         if emu:
-            fn = lib().pccl_emu_hier_reduce_scatter if reduce else lib().pccl_emu_hier_all_gather
-            st = fn(world.handle, N, M, inter, ptr_array([t.data_ptr() for t in sends]),
+            fn = lib().pccl_emu_hier_reduce_scatter_comm if reduce else lib().pccl_emu_hier_all_gather_comm
+            st = fn(comm.handle, N, M, inter, ptr_array([t.data_ptr() for t in sends]),
                     ptr_array([t.data_ptr() for t in recvs]), n, dtype, stream)
         else:
-            fn = lib().pccl_hier_reduce_scatter if reduce else lib().pccl_hier_all_gather
-            st = fn(world.handle, N, M, inter, sends[0].data_ptr(), recvs[0].data_ptr(), n, dtype, stream)
+            fn = lib().pccl_hier_reduce_scatter_comm if reduce else lib().pccl_hier_all_gather_comm
+            st = fn(comm.handle, N, M, inter, sends[0].data_ptr(), recvs[0].data_ptr(), n, dtype, stream)
         check(st, "hier_reduce_scatter" if reduce else "hier_all_gather")
         host = _download([rv for a, rv in zip(args, recvs) if a.host])
         if emu and not host:

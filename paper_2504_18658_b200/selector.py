@@ -8,15 +8,20 @@ Two layers:
   by ``HierPlan.resolve_inter``;
 * a flat selector for ``all_gather(..., algorithm="auto")`` /
   ``reduce_scatter``: a :class:`FlatTable` of *measured* B200 bus bandwidth per
-  (collective, p, message size) — written by ``tools/calibrate.py`` on the GPU
-  box into ``data/flat_calibration.csv`` — with the nearest log-size bucket
-  winning, as in ``CalibrationTable.lookup`` (costmodel.py:127-139).
+  (collective, p, message size) — measured on the GPU box by ``tools/sweep.py``
+  / ``tuning.autotune`` into ``data/flat_calibration.csv`` — with the nearest
+  log-size bucket winning, as in ``CalibrationTable.lookup``
+  (costmodel.py:127-139). A GPU count the table does not cover is calibrated
+  on the live world the first time ``auto`` meets it (``tuning.autotune``,
+  SPMD: every rank measures the same candidates and agrees on the result).
 
-The default ``CostParams`` describe NVLink 5 on B200 (flag round trip a few
-microseconds; 770 GB/s measured peer copy per direction), not the reference's
-desk-scale defaults, but the analytic selector's decisions are the same:
-with equal per-step bandwidth the recursive variant wins exactly when it has
-fewer steps (pow2 N >= 4), and N = 2 ties go to ring.
+``CostParams()`` keeps the reference's desk-scale defaults
+(costmodel.py:35-41), so reference code that evaluates ``t_ring(...,
+CostParams())`` gets the reference's numbers; ``B200_NVLINK`` is the preset
+for NVLink 5 on B200 (flag round trip a few microseconds; 770 GB/s measured
+peer copy per direction). The analytic selector's decisions are the same
+under both: with equal per-step bandwidth the recursive variant wins exactly
+when it has fewer steps (pow2 N >= 4), and N = 2 ties go to ring.
 """
 from __future__ import annotations
 
@@ -37,11 +42,14 @@ def _is_pow2(n: int) -> bool:
 
 @dataclass(frozen=True)
 class CostParams:
-    alpha_inter: float = 3e-6
-    beta_inter: float = 1.0 / 770e9
+    """alpha: seconds per message, beta: seconds per byte, gamma: seconds per
+    reduced byte (costmodel.py:24-41; same defaults)."""
+
+    alpha_inter: float = 10e-6
+    beta_inter: float = 0.04e-9
     alpha_intra: float = 3e-6
-    beta_intra: float = 1.0 / 770e9
-    gamma_reduce_fast: float = 1.0 / 6.5e12
+    beta_intra: float = 0.01e-9
+    gamma_reduce_fast: float = 0.002e-9
     gamma_reduce_slow: float = 0.4e-9
     packet_bytes: int = 2048
 
@@ -59,6 +67,19 @@ class CostParams:
         if level == "intra":
             return self.alpha_intra, self.beta_intra
         raise ValueError(f"unknown level {level!r}")
+
+    def gamma(self, profile: str) -> float:
+        if profile == "fast":
+            return self.gamma_reduce_fast
+        if profile == "slow":
+            return self.gamma_reduce_slow
+        raise ValueError(f"unknown reduce profile {profile!r}")
+
+
+# NVLink 5 / NVSwitch on B200: ~3 us per flag handshake, 770 GB/s measured peer
+# copy per direction (B200_PROFILING.md), 6.5 TB/s HBM for the fused adds
+B200_NVLINK = CostParams(alpha_inter=3e-6, beta_inter=1.0 / 770e9, alpha_intra=3e-6, beta_intra=1.0 / 770e9,
+                         gamma_reduce_fast=1.0 / 6.5e12, gamma_reduce_slow=0.4e-9)
 
 
 def t_ring(p: int, m_bytes: float, params: CostParams, level: str = "inter") -> float:
@@ -79,6 +100,23 @@ def t_direct(p: int, m_bytes: float, params: CostParams, level: str = "intra") -
     """One step: every peer's share moves concurrently over the switch."""
     a, b = params.alpha_beta(level)
     return (a if p > 1 else 0.0) + b * m_bytes * (p - 1) / p
+
+
+def t_hierarchical(topo, m_bytes: float, inter_alg: str, params: CostParams) -> float:
+    """Two-level model (costmodel.py:88-105): the inter phase moves the
+    per-local-rank share m / M across the N nodes, the intra ring moves the
+    whole buffer inside each node; the transpose is free."""
+    n, m_gpus = topo.num_nodes, topo.gpus_per_node
+    sub_m = m_bytes / m_gpus
+    if inter_alg == "auto":
+        inter_alg = choose_inter_algorithm(n, sub_m, params) if n >= 2 else "ring"
+    if inter_alg == "ring":
+        inter = t_ring(n, sub_m, params, level="inter")
+    elif inter_alg == "recursive":
+        inter = t_rec(n, sub_m, params, level="inter")
+    else:
+        raise ValueError(f"unknown inter_alg {inter_alg!r}")
+    return inter + t_ring(m_gpus, m_bytes, params, level="intra")
 
 
 @dataclass(frozen=True)

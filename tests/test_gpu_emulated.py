@@ -465,3 +465,42 @@ def test_hier_block_trace_and_all_ones():
     outs = pkg.run_ranks(4, lambda c: pkg.hier_reduce_scatter(pkg.HierPlan(topo=pkg.Topology(2, 2)), c,
                                                               np.ones(4, np.float32)))
     assert all(np.array_equal(o, [4.0]) for o in outs)
+
+
+@pytest.mark.parametrize("members", [(1, 3, 5, 7), (4, 5, 6, 7), (6, 2, 4, 0)])
+@pytest.mark.parametrize("inter", ["ring", "recursive"])
+def test_hierarchical_on_a_sub_communicator(members, inter):
+    """hierarchy.py:129-134 only requires the communicator's size to match the
+    topology: a 4-member sub-communicator of an 8-rank world runs a 2x2
+    hierarchical AG / RS whose topology rank g is member g."""
+    pkg = _pkg()
+    p, n = len(members), 1000
+    rng = np.random.default_rng(5)
+    ag_in = {m: rng.standard_normal(n).astype(np.float32) for m in members}
+    rs_in = {m: rng.standard_normal(n * p).astype(np.float32) for m in members}
+    plan = pkg.HierPlan(topo=pkg.Topology(2, 2), inter_alg=inter)
+
+    def body(c):
+        sub = c.subgroup(members, 9)
+        if sub is None:
+            return None
+        me = members[sub.rank]
+        return (pkg.hier_all_gather(plan, sub, ag_in[me]), pkg.hier_reduce_scatter(plan, sub, rs_in[me]))
+
+    outs = pkg.run_ranks(8, body)
+    want_ag = oracle.hier_all_gather([ag_in[m] for m in members], 2, 2, inter)
+    want_rs = oracle.hier_reduce_scatter([rs_in[m] for m in members], 2, 2, inter)
+    for w in range(8):
+        if w not in members:
+            assert outs[w] is None
+            continue
+        g = members.index(w)
+        assert _bits_equal(outs[w][0], want_ag[g]), (w, "ag")
+        assert _bits_equal(outs[w][1], want_rs[g]), (w, "rs")
+
+
+def test_hierarchical_world_size_mismatch_raises():
+    pkg = _pkg()
+    plan = pkg.HierPlan(topo=pkg.Topology(2, 2))
+    with pytest.raises(pkg.errors.LengthMismatch):
+        pkg.run_ranks(2, lambda c: pkg.hier_all_gather(plan, c, np.zeros(2, np.float32)))

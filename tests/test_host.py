@@ -223,3 +223,28 @@ def test_pipeline_slices_follow_the_size_knobs(monkeypatch):
     assert C._pipeline_slices(1 << 18, 4, (1 << 20) - 4) is None  # below the threshold
     assert len(C._pipeline_slices(1 << 18, 4, 4 << 20)) == 4
     assert len(C._pipeline_slices(1 << 24, 4, 1 << 30)) == C.PIPE_MAX_SLICES  # capped
+
+
+def test_cost_params_defaults_and_formulas_match_reference():
+    """CostParams() keeps collkit's defaults (costmodel.py:35-41); numbers
+    below were produced by collkit.costmodel in this container."""
+    import math
+
+    from paper_2504_18658_b200 import B200_NVLINK, t_hierarchical
+
+    P = CostParams()
+    assert (P.alpha_inter, P.beta_inter, P.alpha_intra, P.beta_intra) == (10e-6, 0.04e-9, 3e-6, 0.01e-9)
+    assert (P.gamma("fast"), P.gamma("slow"), P.packet_bytes) == (0.002e-9, 0.4e-9, 2048)
+    assert math.isclose(t_ring(8, 1e6, P), 0.000105, rel_tol=1e-12)
+    assert math.isclose(t_rec(8, 1e6, P), 6.500000000000001e-05, rel_tol=1e-12)
+    assert math.isclose(t_ring(4, 2 ** 27, P, "intra"), 0.0010156329599999999, rel_tol=1e-12)
+    for (N, M, alg), want in {(2, 4, "ring"): 0.0033744431999999996, (4, 2, "recursive"): 0.00539170912,
+                              (4, 2, "auto"): 0.00539170912, (2, 4, "auto"): 0.0033744431999999996,
+                              (3, 2, "auto"): 0.004944316693333333}.items():
+        assert math.isclose(t_hierarchical(Topology(N, M, 1), 2 ** 28, alg, P), want, rel_tol=1e-12), (N, M, alg)
+    with pytest.raises(ValueError):
+        t_hierarchical(Topology(2, 2, 1), 1e6, "bogus", P)
+    # the B200 preset changes the numbers, not the analytic decisions
+    for N in (2, 3, 4, 8):
+        for m in (1e3, 1e6, 1e9):
+            assert choose_inter_algorithm(N, m, B200_NVLINK) == choose_inter_algorithm(N, m, P)
