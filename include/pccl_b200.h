@@ -39,6 +39,7 @@ extern "C" {
 
 #define PCCL_MAX_RANKS 16        /* real mode: <= 8 GPUs of one NVSwitch box; emulation: <= 16 */
 #define PCCL_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
+#define PCCL_REG_HANDLE_BYTES 80 /* allocation IPC handle + offset + allocation size */
 
 typedef enum {
   PCCL_SUCCESS = 0,
@@ -114,7 +115,9 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
  * (group size - 1), 0 off), "item_kib" (direct collectives: CTAs claim work
  * items of this many KiB from a device counter instead of static slices;
- * default 0 = static; measured: no gain, see DESIGN). Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
+ * default 0 = static; measured: no gain, see DESIGN), "staged_bytes" (statistic:
+ * bytes of caller buffers that went through staging because they were not in a
+ * registered segment; set 0 to reset). Unknown keys -> PCCL_ERR_INVALID_ARGUMENT. */
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
 int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
 /* With param "trace" = 1, every launch records per-CTA events (globaltimer ns
@@ -129,6 +132,18 @@ int pccl_world_trace_at(pccl_world_t w, int back, uint64_t *host, size_t cap_wor
 /* ---- symmetric segments ---------------------------------------------- */
 int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id);
 int pccl_segment_export(pccl_world_t w, int seg_id, void *handle_out /* PCCL_IPC_HANDLE_BYTES */);
+/* Registration of caller-owned device memory (e.g. a torch caching-allocator
+ * tensor) as a segment, collectively: every rank registers its own buffer of
+ * the same size, exports PCCL_REG_HANDLE_BYTES (the IPC handle of the cudaMalloc
+ * allocation containing it + the offset), the bootstrap exchanges them and
+ * every rank imports all (peer allocations are mapped once per process and
+ * reference counted). Collectives on registered buffers are zero-copy;
+ * pccl_segment_destroy unregisters (the memory stays the caller's). VMM /
+ * expandable-segment memory has no IPC handle: PCCL_ERR_UNSUPPORTED. */
+int pccl_segment_register(pccl_world_t w, void *ptr, size_t bytes, int *seg_id);
+int pccl_segment_register_export(pccl_world_t w, int seg_id, void *handle_out /* PCCL_REG_HANDLE_BYTES */);
+int pccl_segment_register_import(pccl_world_t w, int seg_id, const void *handles /* nranks x REG_HANDLE */);
+int pccl_emu_segment_register(pccl_world_t w, void *const *ptrs /* nranks */, size_t bytes, int *seg_id);
 int pccl_segment_import(pccl_world_t w, int seg_id, const void *handles /* nranks * 64 */);
 int pccl_segment_ptr(pccl_world_t w, int seg_id, int rank, void **ptr, size_t *bytes);
 int pccl_segment_destroy(pccl_world_t w, int seg_id);

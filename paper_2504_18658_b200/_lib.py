@@ -12,6 +12,7 @@ from .errors import STATUS_TO_ERROR, CollkitError
 
 LIB_PATH = os.environ.get("PCCL_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libpccl_b200.so")
 IPC_HANDLE_BYTES = 64
+REG_HANDLE_BYTES = 80  # allocation IPC handle + offset + allocation size
 MAX_RANKS = 16
 
 # pccl_dtype_t / pccl_algo_t / pccl_order_t
@@ -46,6 +47,10 @@ _SIGS = {
     "pccl_segment_export": (_i, [_vp, _i, _vp]),
     "pccl_segment_import": (_i, [_vp, _i, _vp]),
     "pccl_segment_ptr": (_i, [_vp, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_sz)]),
+    "pccl_segment_register": (_i, [_vp, _vp, _sz, ctypes.POINTER(_i)]),
+    "pccl_segment_register_export": (_i, [_vp, _i, _vp]),
+    "pccl_segment_register_import": (_i, [_vp, _i, _vp]),
+    "pccl_emu_segment_register": (_i, [_vp, ctypes.POINTER(_vp), _sz, ctypes.POINTER(_i)]),
     "pccl_segment_destroy": (_i, [_vp, _i]),
     "pccl_world_set_staging": (_i, [_vp, _i]),
     "pccl_staging_bytes": (_sz, [_i, _i, _i, _sz, _i]),

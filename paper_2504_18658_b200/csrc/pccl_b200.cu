@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -19,7 +20,7 @@ using namespace pccl;
 
 namespace {
 
-constexpr int kMaxSegs = 64;
+constexpr int kMaxSegs = 1024;
 
 struct Segment {
   bool used = false;
@@ -27,6 +28,8 @@ struct Segment {
   char *ptr[PCCL_MAXR] = {};      // valid in this process (own, peer-mapped or emulated)
   bool opened[PCCL_MAXR] = {};    // cudaIpcOpenMemHandle'd (must be closed)
   bool owned[PCCL_MAXR] = {};     // cudaMalloc'd here (must be freed)
+  bool reg = false;               // caller-owned memory registered collectively (pccl_segment_register)
+  char *ipc_base[PCCL_MAXR] = {}; // registered: peer allocation base opened through the world's IPC cache
 };
 
 }  // namespace
@@ -73,6 +76,7 @@ struct pccl_world {
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   int64_t p_item_kib = 0;  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
+  int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
@@ -80,6 +84,7 @@ struct pccl_world {
   uint32_t meta_skew[PCCL_MAXR] = {};
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
   std::map<OccKey, int> occ_cache;              // co-resident CTAs per SM, per (kernel, threads, smem)
+  std::map<std::string, std::pair<char *, int>> ipc_open;  // (peer, allocation handle) -> (mapped base, refs)
   std::mutex occ_mu;
 };
 
@@ -551,6 +556,7 @@ struct Binder {
     if (!p) return false;
     fill(r, w->staging, soff, per, p);
     place = place * 31u + 17u;
+    w->p_staged_bytes += (int64_t)bytes;  // staging copy in or out: the buffer was not registered
     if (copy_in && cudaMemcpyAsync(p, user, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) {
       status = PCCL_ERR_CUDA;
       return false;
@@ -1562,6 +1568,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "timeout_ms")) return &w->p_timeout_ms;
   if (!strcmp(key, "trace")) return &w->p_trace;
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
+  if (!strcmp(key, "staged_bytes")) return &w->p_staged_bytes;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
   if (!strcmp(key, "item_kib")) return &w->p_item_kib;
@@ -1671,6 +1678,124 @@ int pccl_segment_import(pccl_world_t w, int seg_id, const void *handles) {
   return PCCL_SUCCESS;
 }
 
+// ---- registration of caller-owned memory (e.g. torch caching-allocator
+// tensors): the peers map the allocation that contains the buffer (CUDA IPC
+// handle of the allocation base + offset), so collectives read / write the
+// registered buffers zero-copy, exactly like World segments.
+static int alloc_seg(pccl_world *w) {
+  for (int i = 1; i < kMaxSegs; ++i)
+    if (!w->segs[i].used) return i;
+  return -1;
+}
+
+int pccl_segment_register(pccl_world_t w, void *ptr, size_t bytes, int *seg_id) {
+  if (!w || w->emu || !ptr || !seg_id) return PCCL_ERR_INVALID_ARGUMENT;
+  const int s = alloc_seg(w);
+  if (s < 0) return PCCL_ERR_OUT_OF_MEMORY;
+  Segment &S = w->segs[s];
+  S = Segment();
+  S.bytes = bytes;
+  S.reg = true;
+  S.ptr[w->rank] = (char *)ptr;
+  S.used = true;
+  *seg_id = s;
+  return PCCL_SUCCESS;
+}
+
+int pccl_emu_segment_register(pccl_world_t w, void *const *ptrs, size_t bytes, int *seg_id) {
+  if (!w || !w->emu || !ptrs || !seg_id) return PCCL_ERR_INVALID_ARGUMENT;
+  const int s = alloc_seg(w);
+  if (s < 0) return PCCL_ERR_OUT_OF_MEMORY;
+  Segment &S = w->segs[s];
+  S = Segment();
+  S.bytes = bytes;
+  S.reg = true;
+  for (int q = 0; q < w->nranks; ++q) {
+    if (!ptrs[q]) return PCCL_ERR_INVALID_ARGUMENT;
+    S.ptr[q] = (char *)ptrs[q];
+  }
+  S.used = true;
+  *seg_id = s;
+  return PCCL_SUCCESS;
+}
+
+using MemGetAddressRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+static MemGetAddressRangeFn mem_range_fn() {
+  static MemGetAddressRangeFn f = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = (MemGetAddressRangeFn)fp;
+    else
+      cudaGetLastError();
+  });
+  return f;
+}
+
+int pccl_segment_register_export(pccl_world_t w, int seg_id, void *handle_out) {
+  if (!w || w->emu || seg_id <= 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || !w->segs[seg_id].reg ||
+      !handle_out)
+    return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  MemGetAddressRangeFn range = mem_range_fn();
+  if (!range) return PCCL_ERR_UNSUPPORTED;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  char *p = w->segs[seg_id].ptr[w->rank];
+  if (range(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) return PCCL_ERR_INVALID_ARGUMENT;  // not device memory
+  if ((char *)base + size < p + w->segs[seg_id].bytes) return PCCL_ERR_INVALID_ARGUMENT;     // spans allocations
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, (void *)base) != cudaSuccess) {  // e.g. VMM / expandable-segment memory
+    cudaGetLastError();
+    return PCCL_ERR_UNSUPPORTED;
+  }
+  const uint64_t off = (uint64_t)(p - (char *)base), sz = (uint64_t)size;
+  memcpy(handle_out, &h, sizeof(h));
+  memcpy((char *)handle_out + PCCL_IPC_HANDLE_BYTES, &off, 8);
+  memcpy((char *)handle_out + PCCL_IPC_HANDLE_BYTES + 8, &sz, 8);
+  return PCCL_SUCCESS;
+}
+
+int pccl_segment_register_import(pccl_world_t w, int seg_id, const void *handles) {
+  if (!w || w->emu || seg_id <= 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || !w->segs[seg_id].reg ||
+      !handles)
+    return PCCL_ERR_INVALID_ARGUMENT;
+  CK(cudaSetDevice(w->device));
+  Segment &S = w->segs[seg_id];
+  for (int q = 0; q < w->nranks; ++q) {
+    if (q == w->rank || S.ptr[q]) continue;
+    const char *hq = (const char *)handles + (size_t)q * PCCL_REG_HANDLE_BYTES;
+    uint64_t off = 0;
+    memcpy(&off, hq + PCCL_IPC_HANDLE_BYTES, 8);
+    std::string key((const char *)&q, sizeof(q));
+    key.append(hq, PCCL_IPC_HANDLE_BYTES);
+    auto it = w->ipc_open.find(key);
+    char *base = nullptr;
+    if (it != w->ipc_open.end()) {
+      base = it->second.first;
+      it->second.second++;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, hq, sizeof(h));
+      void *b = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        fprintf(stderr, "[pccl_b200] rank %d cannot map registered buffer of rank %d: %s\n", w->rank, q,
+                cudaGetErrorString(e));
+        return PCCL_ERR_PEER_UNREACHABLE;
+      }
+      base = (char *)b;
+      w->ipc_open[key] = {base, 1};
+    }
+    S.ipc_base[q] = base;
+    S.ptr[q] = base + off;
+  }
+  return PCCL_SUCCESS;
+}
+
 int pccl_segment_ptr(pccl_world_t w, int seg_id, int rank, void **ptr, size_t *bytes) {
   if (!w || seg_id < 0 || seg_id >= kMaxSegs || !w->segs[seg_id].used || rank < 0 || rank >= w->nranks)
     return PCCL_ERR_INVALID_ARGUMENT;
@@ -1687,6 +1812,16 @@ int pccl_segment_destroy(pccl_world_t w, int seg_id) {
   for (int q = 0; q < w->nranks; ++q) {
     if (S.opened[q]) cudaIpcCloseMemHandle(S.ptr[q]);
     if (S.owned[q]) cudaFree(S.ptr[q]);
+    if (S.ipc_base[q]) {  // registered: drop this segment's reference on the peer allocation's mapping
+      for (auto it = w->ipc_open.begin(); it != w->ipc_open.end(); ++it)
+        if (it->second.first == S.ipc_base[q]) {
+          if (--it->second.second == 0) {
+            cudaIpcCloseMemHandle(it->second.first);
+            w->ipc_open.erase(it);
+          }
+          break;
+        }
+    }
   }
   S = Segment();
   if (w->staging == seg_id) w->staging = -1;

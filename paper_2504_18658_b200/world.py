@@ -28,7 +28,8 @@ from typing import Callable
 import torch
 
 from . import _lib
-from ._lib import check, lib
+from ._lib import check, lib, ptr_array
+from .errors import OutOfMemory
 
 TORCH_DTYPES = {
     torch.float32: "f32",
@@ -55,6 +56,22 @@ class _CudaArray:
         }
 
 
+class _Lease:
+    """Lifetime of memory handed out as tensors (World.empty / SymmetricHeap):
+    the tensors' storages keep it alive; when the last one dies the release
+    callback is queued on the world and run at the next allocation outside
+    CUDA-graph capture (it synchronises the device)."""
+
+    def __init__(self, world: "World", release: Callable[[], None]):
+        self._world = world
+        self._release = release
+
+    def __del__(self):  # pragma: no cover - GC timing
+        w = self._world
+        if w is not None and not w._closed:
+            w._pending.append(self._release)
+
+
 class Segment:
     def __init__(self, world: "World", seg_id: int, nbytes: int):
         self.world = world
@@ -66,12 +83,94 @@ class Segment:
         check(lib().pccl_segment_ptr(self.world.handle, self.id, rank, ctypes.byref(p), None), "segment_ptr")
         return p.value or 0
 
-    def tensor(self, rank: int, offset: int = 0, nbytes: int | None = None) -> torch.Tensor:
+    def tensor(self, rank: int, offset: int = 0, nbytes: int | None = None, owner=None) -> torch.Tensor:
         """uint8 tensor over [offset, offset + nbytes) of rank's copy (this
-        process must own it: its own rank in real mode, any rank in emulation)."""
+        process must own it: its own rank in real mode, any rank in emulation).
+        ``owner`` is kept alive by the tensor's storage."""
         nbytes = self.nbytes - offset if nbytes is None else nbytes
-        base = torch.as_tensor(_CudaArray(self.ptr(rank), self.nbytes, self), device=f"cuda:{self.world.device}")
-        return base[offset : offset + nbytes]
+        base = torch.as_tensor(_CudaArray(self.ptr(rank) + offset, nbytes, owner or self),
+                               device=f"cuda:{self.world.device}")
+        return base
+
+
+class Registration:
+    """Caller-owned tensors registered collectively as a segment (zero-copy
+    for collectives whose buffers lie inside it). Keeps the tensors alive
+    until ``close()``."""
+
+    def __init__(self, world: "World", seg: Segment, tensors):
+        self.world, self.segment, self._tensors = world, seg, tensors
+
+    def close(self) -> None:
+        if self.segment is not None and not self.world._closed:
+            self.world.destroy_segment(self.segment)
+        self.segment, self._tensors = None, None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class SymmetricHeap:
+    """A symmetric arena (one collective segment) with a deterministic
+    first-fit allocator: as long as every rank performs the same sequence of
+    ``empty`` calls and tensor releases (SPMD code, e.g. FSDP), a block lands
+    at the same offset on every rank, so collectives on heap tensors are
+    zero-copy. A divergence is not silent: the offset enters every call's
+    signature and mismatched ranks raise LengthMismatch. Freed blocks are
+    reused in address order; reuse is stream-ordered like the caching
+    allocator's (a block freed while another stream still uses it needs the
+    usual event / record_stream discipline)."""
+
+    ALIGN = 256
+
+    def __init__(self, world: "World", nbytes: int):
+        self.world = world
+        self.segment = world.create_segment(nbytes)
+        self.nbytes = self.segment.nbytes
+        self._free = [(0, self.nbytes)]  # sorted (offset, size)
+        self._lock = threading.Lock()
+
+    def _alloc(self, size: int) -> int:
+        size = max(self.ALIGN, (size + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
+        with self._lock:
+            for i, (off, sz) in enumerate(self._free):
+                if sz >= size:
+                    if sz == size:
+                        self._free.pop(i)
+                    else:
+                        self._free[i] = (off + size, sz - size)
+                    return off, size
+        raise OutOfMemory(f"symmetric heap: no free block of {size} bytes ({self.nbytes} total)")
+
+    def _release(self, off: int, size: int) -> None:
+        with self._lock:
+            self._free.append((off, size))
+            self._free.sort()
+            merged = []
+            for o, z in self._free:
+                if merged and merged[-1][0] + merged[-1][1] == o:
+                    merged[-1] = (merged[-1][0], merged[-1][1] + z)
+                else:
+                    merged.append((o, z))
+            self._free = merged
+
+    def empty(self, numel: int, dtype=torch.float32):
+        """This rank's tensor (real mode) or one per rank (emulation)."""
+        self.world._run_pending()
+        es = torch.empty(0, dtype=dtype).element_size()
+        off, size = self._alloc(numel * es)
+        heap = self
+        lease = _Lease(self.world, lambda: heap._release(off, size))
+        if self.world.emulated:
+            return [self.segment.tensor(r, off, numel * es, lease).view(dtype) for r in range(self.world.nranks)]
+        return self.segment.tensor(self.world.rank, off, numel * es, lease).view(dtype)
+
+    def bytes_free(self) -> int:
+        with self._lock:
+            return sum(z for _, z in self._free)
 
 
 class World:
@@ -86,6 +185,7 @@ class World:
         self.emulated = emulated
         self._exchange = exchange
         self._segments: dict[int, Segment] = {}
+        self._pending: list = []  # releases queued by dead leases (run outside graph capture)
         self.staging: Segment | None = None
         self.io: Segment | None = None
         self.lock = threading.RLock()
@@ -122,8 +222,16 @@ class World:
         self._segments[seg_id] = seg
         return seg
 
+    def _run_pending(self) -> None:
+        if not self._pending or torch.cuda.is_current_stream_capturing():
+            return
+        todo, self._pending = self._pending, []
+        for release in todo:
+            release()
+
     def create_segment(self, nbytes: int) -> Segment:
         """Collective (real mode): allocate nbytes on every rank and map them."""
+        self._run_pending()
         sid = ctypes.c_int(-1)
         check(lib().pccl_segment_create(self.handle, nbytes, ctypes.byref(sid)), "segment_create")
         return self._share(sid.value, nbytes)
@@ -161,12 +269,57 @@ class World:
     def empty(self, numel: int, dtype=torch.float32, rank: int | None = None):
         """Symmetric tensor(s) peers can read zero-copy. Collective in real
         mode (returns this rank's tensor); in emulation returns one tensor per
-        rank."""
+        rank. The segment is released (collectively: every rank drops its
+        tensors in the same program order) once its tensors are gone."""
         es = torch.empty(0, dtype=dtype).element_size()
         seg = self.create_segment(max(256, numel * es))
+        lease = _Lease(self, lambda: self.destroy_segment(seg) if seg.id in self._segments else None)
         if self.emulated:
-            return [seg.tensor(r, 0, numel * es).view(dtype) for r in range(self.nranks)]
-        return seg.tensor(self.rank, 0, numel * es).view(dtype)
+            return [seg.tensor(r, 0, numel * es, lease).view(dtype) for r in range(self.nranks)]
+        return seg.tensor(self.rank, 0, numel * es, lease).view(dtype)
+
+    def heap(self, nbytes: int) -> SymmetricHeap:
+        """A symmetric arena with a deterministic allocator (collective)."""
+        return SymmetricHeap(self, nbytes)
+
+    def register(self, tensor) -> Registration:
+        """Register caller-owned CUDA tensor(s) for zero-copy collectives.
+        Collective in real mode: every rank passes its own tensor of the same
+        byte size (the peers map the cudaMalloc allocation that contains it;
+        torch's caching allocator qualifies, expandable segments do not ->
+        Unsupported). Emulation: a list with one tensor per rank."""
+        self._run_pending()
+        ts = list(tensor) if self.emulated else [tensor]
+        if self.emulated and len(ts) != self.nranks:
+            raise ValueError(f"emulation: register one tensor per rank ({self.nranks})")
+        for t in ts:
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+                raise ValueError("register: contiguous CUDA tensors only")
+        nbytes = ts[0].numel() * ts[0].element_size()
+        sid = ctypes.c_int(-1)
+        if self.emulated:
+            check(lib().pccl_emu_segment_register(self.handle, ptr_array([t.data_ptr() for t in ts]), nbytes,
+                                                  ctypes.byref(sid)), "segment_register")
+        else:
+            check(lib().pccl_segment_register(self.handle, ts[0].data_ptr(), nbytes, ctypes.byref(sid)),
+                  "segment_register")
+            try:
+                buf = (ctypes.c_char * _lib.REG_HANDLE_BYTES)()
+                st = lib().pccl_segment_register_export(self.handle, sid.value, buf)
+                blobs = self._exchange(bytes([st & 0xff]) + bytes(buf))
+                bad = [b[0] for b in blobs if b[0]]
+                if bad:  # every rank fails the same way (no one imports)
+                    check(bad[0], "segment_register_export")
+                allh = (ctypes.c_char * (_lib.REG_HANDLE_BYTES * self.nranks))()
+                for q, hb in enumerate(blobs):
+                    ctypes.memmove(ctypes.addressof(allh) + q * _lib.REG_HANDLE_BYTES, hb[1:], _lib.REG_HANDLE_BYTES)
+                check(lib().pccl_segment_register_import(self.handle, sid.value, allh), "segment_register_import")
+            except Exception:
+                lib().pccl_segment_destroy(self.handle, sid.value)
+                raise
+        seg = Segment(self, sid.value, nbytes)
+        self._segments[sid.value] = seg
+        return Registration(self, seg, ts)
 
     # ---- status --------------------------------------------------------
     def check(self) -> None:

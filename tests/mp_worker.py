@@ -339,6 +339,44 @@ def main() -> int:
         del grad, gsh
         sync_point("fullsize")
 
+    # zero-copy for torch-owned tensors: register caching-allocator buffers
+    # collectively (CUDA IPC of the containing allocation + offset), then the
+    # collectives bind them without staging; and the symmetric heap
+    w = comm.world
+    n = 300_001
+    xr = torch.randn(n * p, device="cuda")
+    yr = torch.empty(n, device="cuda")
+    zr = torch.empty(n * p, device="cuda")
+    with w.register(xr), w.register(yr), w.register(zr):
+        w.set_param("staged_bytes", 0)
+        all_x = [torch.empty_like(xr) for _ in range(p)]
+        dist.all_gather(all_x, xr)
+        for algo in ["direct", "ring"] + (["recursive"] if pow2 else []):
+            order = "recursive" if algo == "recursive" else "ring"
+            pkg.reduce_scatter(comm, xr, algorithm=algo, order=order, out=yr)
+            want = oracle.rechalf_reduce_scatter([a.cpu().numpy() for a in all_x])[rank] if algo == "recursive" \
+                else oracle.ring_reduce_scatter([a.cpu().numpy() for a in all_x])[rank]
+            check(f"registered_rs_{algo}", yr.cpu().numpy(), want)
+            pkg.all_gather(comm, yr, algorithm=algo, out=zr)
+            all_y = [torch.empty_like(yr) for _ in range(p)]
+            dist.all_gather(all_y, yr)
+            check(f"registered_ag_{algo}", zr.cpu().numpy(), torch.cat(all_y).cpu().numpy())
+        torch.cuda.synchronize()
+        if w.get_param("staged_bytes") != 0:
+            failures.append(f"registered buffers staged {w.get_param('staged_bytes')} B")
+    heap = w.heap(64 << 20)
+    a = heap.empty(n * p, torch.float32)
+    b = heap.empty(n, torch.float32)
+    a.copy_(xr)
+    w.set_param("staged_bytes", 0)
+    pkg.reduce_scatter(comm, a, algorithm="direct", out=b)
+    torch.cuda.synchronize()
+    check("heap_rs_direct", b.cpu().numpy(), oracle.ring_reduce_scatter([t.cpu().numpy() for t in all_x])[rank])
+    if w.get_param("staged_bytes") != 0:
+        failures.append("heap buffers staged")
+    del a, b
+    sync_point("registration")
+
     # online calibration: every rank must resolve "auto" identically afterwards
     from paper_2504_18658_b200 import selector, tuning
 

@@ -504,3 +504,83 @@ def test_hierarchical_world_size_mismatch_raises():
     plan = pkg.HierPlan(topo=pkg.Topology(2, 2))
     with pytest.raises(pkg.errors.LengthMismatch):
         pkg.run_ranks(2, lambda c: pkg.hier_all_gather(plan, c, np.zeros(2, np.float32)))
+
+
+def test_registered_torch_tensors_are_zero_copy():
+    """World.register (emulation: one caching-allocator tensor per rank):
+    collectives bind the registered buffers without staging and stay exact."""
+    pkg = _pkg()
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    p, n = 4, 70001
+    w = emulated_world(p, 0)
+    rng = np.random.default_rng(11)
+    ins = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    xs = [torch.from_numpy(x).cuda() for x in ins]
+    ys = [torch.empty(n, device="cuda") for _ in range(p)]
+    zs = [torch.empty(n * p, device="cuda") for _ in range(p)]
+    with w.register(xs), w.register(ys), w.register(zs):
+        w.set_param("staged_bytes", 0)
+        for algo in ("direct", "ring", "recursive"):
+            order = "recursive" if algo == "recursive" else "ring"
+            pkg.run_ranks(p, lambda c: pkg.reduce_scatter(c, xs[c.rank], algorithm=algo, order=order, out=ys[c.rank]))
+            want = oracle.rechalf_reduce_scatter(ins) if algo == "recursive" else oracle.ring_reduce_scatter(ins)
+            for r in range(p):
+                assert _bits_equal(ys[r].cpu().numpy(), want[r]), (algo, r)
+            pkg.run_ranks(p, lambda c: pkg.all_gather(c, ys[c.rank], algorithm=algo, out=zs[c.rank]))
+            for r in range(p):
+                assert _bits_equal(zs[r].cpu().numpy(), np.concatenate([y.cpu().numpy() for y in ys])), (algo, r)
+        torch.cuda.synchronize()
+        assert w.get_param("staged_bytes") == 0
+    # after close() the same tensors are staged again (counter moves)
+    pkg.run_ranks(p, lambda c: pkg.reduce_scatter(c, xs[c.rank], algorithm="direct", out=ys[c.rank]))
+    torch.cuda.synchronize()
+    assert w.get_param("staged_bytes") > 0
+
+
+def test_symmetric_heap_allocates_deterministically_and_reuses():
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    pkg = _pkg()
+    p = 4
+    w = emulated_world(p, 0)
+    heap = w.heap(8 << 20)
+    free0 = heap.bytes_free()
+    a = heap.empty(1000, torch.float32)
+    b = heap.empty(3000, torch.bfloat16)
+    assert len(a) == p and a[0].data_ptr() - heap.segment.ptr(0) == 0
+    assert b[0].data_ptr() - heap.segment.ptr(0) == 4096  # 4000 B rounded to 256
+    for r in range(p):  # every rank's block at the same offset
+        assert a[r].data_ptr() - heap.segment.ptr(r) == 0 and b[r].data_ptr() - heap.segment.ptr(r) == 4096
+    x = heap.empty(4096 * p, torch.float32)
+    y = heap.empty(4096, torch.float32)
+    for r in range(p):
+        x[r].fill_(float(r + 1))
+    w.set_param("staged_bytes", 0)
+    pkg.run_ranks(p, lambda c: pkg.reduce_scatter(c, x[c.rank], algorithm="direct", out=y[c.rank]))
+    torch.cuda.synchronize()
+    assert w.get_param("staged_bytes") == 0
+    assert all(float(y[r][0]) == p * (p + 1) / 2 for r in range(p))
+    del a, b, x, y
+    import gc
+
+    gc.collect()
+    heap.empty(16, torch.float32)  # runs the queued releases
+    assert heap.bytes_free() == free0 - 256
+    with pytest.raises(pkg.errors.OutOfMemory):
+        heap.empty(16 << 20, torch.float32)
+
+
+def test_world_empty_segments_are_released():
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    w = emulated_world(2, 0)
+    before = len(w._segments)
+    for _ in range(100):  # more than the old 64-segment table without releases
+        t = w.empty(1 << 16, torch.float32)
+        del t
+    import gc
+
+    gc.collect()
+    w._run_pending()
+    assert len(w._segments) <= before + 1

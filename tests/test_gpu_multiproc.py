@@ -64,3 +64,20 @@ def test_real_mode_fuzz(nproc):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count("FUZZ OK") == nproc, out[-4000:]
+
+
+def test_fsdp2_with_b200_collectives_matches_nccl():
+    """FSDP2 (fully_shard) with the B200 all-gather / reduce-scatter installed
+    through paper_2504_18658_b200.fsdp: a two-layer 7B-shape model (h = 4096)
+    at the largest power-of-two GPU count available (<= 4); parameters and
+    loss bit-identical to NCCL's, gradients within the bf16 bound, nothing
+    staged (tests/mp_fsdp.py)."""
+    n = 4 if _ngpus() >= 4 else 2
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29547", os.path.join(ROOT, "tests", "mp_fsdp.py")]
+    r = subprocess.run(cmd, env=dict(os.environ, PCCL_TIMEOUT_MS="60000"), capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count(" OK") == n, out[-4000:]
