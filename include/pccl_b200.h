@@ -177,6 +177,19 @@ int pccl_all_gather(pccl_comm_t c, int algo, const void *send, void *recv, size_
 int pccl_reduce_scatter(pccl_comm_t c, int algo, int order, const void *send, void *recv, size_t recvcount,
                         int dtype, void *stream);
 
+/* ---- point-to-point (transport/base.py:140-152) ----------------------------
+ * Tagged messages between group ranks with exact (source, tag) FIFO matching.
+ * pccl_send returns once the message sits in the destination's mailbox ring
+ * (it never waits for a matching receive; with a full ring it drains its own
+ * incoming rings while waiting, so symmetric exchanges cannot deadlock).
+ * pccl_recv blocks until a message from `src` with `tag` is complete; buf ==
+ * NULL probes (returns its size in *bytes and leaves it queued); a buffer
+ * smaller than the message -> PCCL_ERR_LENGTH_MISMATCH (message kept). `host`
+ * = 1: buf is host memory. `me` is the caller's group rank (real mode: must
+ * be this process's). Host-driven control path, timeout = the world timeout. */
+int pccl_send(pccl_comm_t c, int me, int dst, int64_t tag, const void *buf, size_t bytes, int host);
+int pccl_recv(pccl_comm_t c, int me, int src, int64_t tag, void *buf, size_t cap, int host, size_t *bytes);
+
 /* ---- hierarchical (hierarchy.py:158-195), world of N x M virtual nodes --- */
 int pccl_hier_all_gather(pccl_world_t w, int N, int M, int inter_algo, const void *send, void *recv, size_t count,
                          int dtype, void *stream);

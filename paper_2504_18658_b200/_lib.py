@@ -59,6 +59,8 @@ _SIGS = {
     "pccl_comm_size": (_i, [_vp, ctypes.POINTER(_i)]),
     "pccl_comm_rank": (_i, [_vp, ctypes.POINTER(_i)]),
     "pccl_comm_epoch": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_uint64)]),
+    "pccl_send": (_i, [_vp, _i, _i, ctypes.c_int64, _vp, _sz, _i]),
+    "pccl_recv": (_i, [_vp, _i, _i, ctypes.c_int64, _vp, _sz, _i, ctypes.POINTER(_sz)]),
     "pccl_all_gather": (_i, [_vp, _i, _vp, _vp, _sz, _i, _vp]),
     "pccl_reduce_scatter": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _vp]),
     "pccl_hier_all_gather": (_i, [_vp, _i, _i, _i, _vp, _vp, _sz, _i, _vp]),

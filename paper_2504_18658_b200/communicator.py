@@ -194,17 +194,58 @@ class Communicator:
             return Communicator(self.world, members, comm_id, rank=self.world_rank, _group=group, _rdv=rdv)
         return Communicator(self.world, members, comm_id)
 
-    # -- point-to-point is not part of this path ------------------------------
-    def send(self, dst, tag, payload):  # pragma: no cover - documented gap
-        raise Unsupported("point-to-point send is not part of the B200 collective path")
+    # -- point-to-point (transport/base.py:140-152) ---------------------------
+    # Tagged messages over per-pair mailbox rings in the flag arena (C ABI
+    # pccl_send / pccl_recv): exact (source, tag) FIFO matching; send never
+    # waits for a matching recv. Payloads: bytes-like (host) or CUDA tensors.
+    def send(self, dst: int, tag: int, payload) -> None:
+        if not 0 <= dst < self.size:
+            raise IndexOutOfRange(f"destination {dst} not in [0, {self.size})")
+        if dst == self.rank:  # transport contract (inprocess.py, tests/test_transport_inprocess.py)
+            raise SelfSend(f"rank {self.rank} cannot send to itself")
+        if tag < 0:
+            raise ValueError(f"tag must be >= 0, got {tag}")
+        keep = None
+        if isinstance(payload, torch.Tensor) and payload.is_cuda:
+            t = payload.contiguous()
+            ptr, nbytes, host, keep = t.data_ptr(), t.numel() * t.element_size(), 0, t
+        else:
+            if isinstance(payload, torch.Tensor):
+                payload = payload.contiguous().numpy()
+            mv = memoryview(payload).cast("B")
+            nbytes = mv.nbytes
+            if nbytes % 4:  # payloads are whole fp32 elements (transport/base.py:46)
+                raise LengthMismatch(f"payload of {nbytes} bytes is not a whole number of 4-byte elements")
+            keep = (ctypes.c_char * max(nbytes, 1)).from_buffer_copy(mv) if nbytes else None
+            ptr, host = (ctypes.addressof(keep) if keep is not None else None), 1
+        check(lib().pccl_send(self.handle, self.rank, dst, int(tag), ptr, nbytes, host), "send")
+        del keep
 
-    def recv(self, src, tag):  # pragma: no cover
-        raise Unsupported("point-to-point recv is not part of the B200 collective path")
+    def recv(self, src: int, tag: int) -> bytes:
+        if not 0 <= src < self.size:
+            raise IndexOutOfRange(f"source {src} not in [0, {self.size})")
+        n = ctypes.c_size_t(0)
+        check(lib().pccl_recv(self.handle, self.rank, src, int(tag), None, 0, 1, ctypes.byref(n)), "recv")
+        buf = (ctypes.c_char * max(n.value, 1))()
+        check(lib().pccl_recv(self.handle, self.rank, src, int(tag), buf, n.value, 1, ctypes.byref(n)), "recv")
+        return bytes(buf[: n.value])
 
-    def sendrecv(self, peer, tag, payload):  # pragma: no cover
+    def recv_into(self, src: int, tag: int, out: torch.Tensor) -> torch.Tensor:
+        """Receive straight into a CUDA tensor (its byte size must hold the message)."""
+        if not (out.is_cuda and out.is_contiguous()):
+            raise ValueError("recv_into: contiguous CUDA tensor required")
+        n = ctypes.c_size_t(0)
+        check(lib().pccl_recv(self.handle, self.rank, src, int(tag), out.data_ptr(), out.numel() * out.element_size(),
+                              0, ctypes.byref(n)), "recv")
+        return out
+
+    def sendrecv(self, peer: int, tag: int, payload) -> bytes:
+        """Exchange with one peer; no deadlock whatever the peer's ordering
+        (sends never wait for the receiver, base.py:143-149)."""
         if peer == self.rank:
             raise SelfSend(f"rank {self.rank} cannot exchange with itself")
-        raise Unsupported("point-to-point sendrecv is not part of the B200 collective path")
+        self.send(peer, tag, payload)
+        return self.recv(peer, tag)
 
 
 # ---------------------------------------------------------------------------

@@ -44,7 +44,16 @@
 #define PCCL_LL_HDR_BYTES 256
 #define PCCL_LL_MAX_PAYLOAD ((size_t)1 << 20)  // payload bytes per (src -> dst) message
 #define PCCL_LL_REGION_BYTES (PCCL_LL_HDR_BYTES + 2 * PCCL_LL_MAX_PAYLOAD)
-#define PCCL_FLAG_BYTES (PCCL_LL_OFF * 8 + (size_t)2 * PCCL_MAXR * PCCL_LL_REGION_BYTES)
+// After the LL regions: the point-to-point mailboxes (host-driven send / recv,
+// see "point-to-point" in pccl_b200.cu): per source rank one ring of
+// PCCL_MBOX_BYTES in the receiver's arena. WCTRL words [16 + s]: bytes rank s
+// has written into my ring (its head); [32 + d]: bytes rank d has consumed of
+// my messages (my tail at d).
+#define PCCL_MBOX_OFF ((PCCL_LL_OFF * 8 + (size_t)2 * PCCL_MAXR * PCCL_LL_REGION_BYTES + 4095) & ~(size_t)4095)  // bytes
+#define PCCL_MBOX_BYTES ((size_t)2 << 20)
+#define PCCL_WCTRL_HEAD 16
+#define PCCL_WCTRL_TAIL 32
+#define PCCL_FLAG_BYTES (PCCL_MBOX_OFF + (size_t)PCCL_MAXR * PCCL_MBOX_BYTES)
 #define PCCL_ABORT_BIT (1ull << 63)
 
 namespace pccl {

@@ -13,6 +13,9 @@
 #include <map>
 #include <string>
 #include <mutex>
+#include <deque>
+#include <thread>
+#include <chrono>
 #include <type_traits>
 #include <vector>
 
@@ -41,6 +44,23 @@ struct OccKey {
   bool operator<(const OccKey &o) const {
     return k != o.k ? k < o.k : threads != o.threads ? threads < o.threads : smem < o.smem;
   }
+};
+
+// Point-to-point state of one world rank executed by this process.
+struct P2PMsg {
+  int64_t tag = 0;
+  size_t bytes = 0;
+  char *dev = nullptr;  // cudaMalloc'd copy (complete message), nullptr when bytes == 0
+  size_t have = 0;      // fragment assembly: bytes received so far
+};
+struct P2PRank {
+  uint64_t head_sent[PCCL_MAXR] = {};  // bytes I wrote into rank q's ring from me
+  uint64_t tail_read[PCCL_MAXR] = {};  // bytes I consumed from my ring of source q
+  std::deque<P2PMsg> unexpected[PCCL_MAXR];  // complete messages from source q, arrival order
+  P2PMsg partial[PCCL_MAXR];                 // message from q being assembled (fragments)
+  bool in_partial[PCCL_MAXR] = {};
+  cudaStream_t stream = nullptr;
+  char *hdr = nullptr;  // pinned 64-byte scratch
 };
 
 struct pccl_world {
@@ -85,6 +105,7 @@ struct pccl_world {
   std::map<uint32_t, pccl_comm *> comm_cache;  // hierarchical sub-groups
   std::map<OccKey, int> occ_cache;              // co-resident CTAs per SM, per (kernel, threads, smem)
   std::map<std::string, std::pair<char *, int>> ipc_open;  // (peer, allocation handle) -> (mapped base, refs)
+  P2PRank p2p[PCCL_MAXR];  // indexed by world rank (real mode: own rank only)
   std::mutex occ_mu;
 };
 
@@ -1426,6 +1447,198 @@ int pccl_nvls_reduce_scatter(pccl_comm_t c, int id, size_t in_offset, void *recv
 
 
 // ============================================================================
+// Point-to-point (transport/base.py:140-152): tagged messages with exact
+// (source, tag) FIFO matching, sends that never wait for a matching receive.
+// Each (source -> dest) pair owns a ring of PCCL_MBOX_BYTES in the dest's
+// flag arena (mapped by every peer). The sender copies a 64-byte frame header
+// and the payload into the ring (copy engine, peer memory), then publishes
+// its head (bytes written) in the dest's WCTRL word; the receiver drains every
+// ring into complete-message buffers in arrival order (so a message waiting
+// for its tag never blocks the ring) and publishes its tail (bytes consumed)
+// in the sender's WCTRL word. A sender short of ring space drains its own
+// incoming rings while it waits, so two ranks exchanging messages larger than
+// a ring make progress (sendrecv). Messages larger than a ring travel as
+// fragments. Host-driven: this path carries control traffic, never the
+// collectives' data.
+// ============================================================================
+namespace {
+
+constexpr uint64_t kFrameMagic = 0x50434C4C50325000ull;  // "PCLLP2P"
+struct Frame {
+  uint64_t magic, kind;  // kind 0: message fragment, 1: skip to the ring's end
+  int64_t tag;
+  uint64_t total, off, len;
+  uint64_t pad[2];
+};
+static_assert(sizeof(Frame) == 64, "frame header is 64 bytes");
+
+char *arena(pccl_world *w, int q) { return w->segs[0].ptr[q]; }
+uint64_t *wctrl(pccl_world *w, int q, int idx) {
+  return (uint64_t *)arena(w, q) + PCCL_WCTRL_OFF + idx;
+}
+char *ring(pccl_world *w, int dst, int src) { return arena(w, dst) + PCCL_MBOX_OFF + (size_t)src * PCCL_MBOX_BYTES; }
+
+int p2p_init(pccl_world *w, int me) {
+  P2PRank &pr = w->p2p[me];
+  if (!pr.stream) CK(cudaStreamCreateWithFlags(&pr.stream, cudaStreamNonBlocking));
+  if (!pr.hdr) CK(cudaHostAlloc((void **)&pr.hdr, 64, cudaHostAllocDefault));
+  return PCCL_SUCCESS;
+}
+uint64_t read_word(const uint64_t *dev) {
+  uint64_t v = 0;
+  cudaMemcpy(&v, dev, 8, cudaMemcpyDeviceToHost);
+  return v;
+}
+int write_word(uint64_t *dev, uint64_t v) {
+  CK(cudaMemcpy(dev, &v, 8, cudaMemcpyHostToDevice));
+  return PCCL_SUCCESS;
+}
+
+// Drain every ring of `me` into complete messages; publish the tails.
+int p2p_progress(pccl_world *w, int me) {
+  P2PRank &pr = w->p2p[me];
+  for (int src = 0; src < w->nranks; ++src) {
+    if (src == me) continue;
+    const uint64_t head = read_word(wctrl(w, me, PCCL_WCTRL_HEAD + src));
+    const uint64_t start = pr.tail_read[src];
+    while (pr.tail_read[src] < head) {
+      const size_t pos = pr.tail_read[src] % PCCL_MBOX_BYTES;
+      Frame f;
+      CK(cudaMemcpy(&f, ring(w, me, src) + pos, sizeof(f), cudaMemcpyDeviceToHost));
+      if (f.magic != kFrameMagic) return PCCL_ERR_CUDA;  // corrupted ring: never expected
+      if (f.kind == 1) {
+        pr.tail_read[src] += PCCL_MBOX_BYTES - pos;
+        continue;
+      }
+      P2PMsg &m = pr.partial[src];
+      if (!pr.in_partial[src]) {
+        m = P2PMsg();
+        m.tag = f.tag;
+        m.bytes = f.total;
+        if (f.total) CK(cudaMalloc((void **)&m.dev, f.total));
+        pr.in_partial[src] = true;
+      }
+      if (f.len) CK(cudaMemcpy(m.dev + f.off, ring(w, me, src) + pos + 64, f.len, cudaMemcpyDeviceToDevice));
+      m.have += f.len;
+      pr.tail_read[src] += 64 + ((f.len + 63) & ~(uint64_t)63);
+      if (m.have == m.bytes) {
+        pr.unexpected[src].push_back(m);
+        pr.in_partial[src] = false;
+        m = P2PMsg();
+      }
+    }
+    if (pr.tail_read[src] != start) {
+      const int s = write_word(wctrl(w, src, PCCL_WCTRL_TAIL + me), pr.tail_read[src]);
+      if (s) return s;
+    }
+  }
+  return PCCL_SUCCESS;
+}
+
+int p2p_send(pccl_world *w, int me, int dst, int64_t tag, const void *buf, size_t bytes, bool host) {
+  int s = p2p_init(w, me);
+  if (s) return s;
+  P2PRank &pr = w->p2p[me];
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (dst == me) {  // self-send: straight into my own queue
+    P2PMsg m;
+    m.tag = tag;
+    m.bytes = m.have = bytes;
+    if (bytes) {
+      CK(cudaMalloc((void **)&m.dev, bytes));
+      CK(cudaMemcpy(m.dev, buf, bytes, kind));
+    }
+    pr.unexpected[me].push_back(m);
+    return PCCL_SUCCESS;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  auto wait_space = [&](uint64_t need) -> int {
+    while (true) {
+      const uint64_t tail = read_word(wctrl(w, me, PCCL_WCTRL_TAIL + dst));
+      if (PCCL_MBOX_BYTES - (pr.head_sent[dst] - tail) >= need) return PCCL_SUCCESS;
+      const int e = p2p_progress(w, me);  // keep my own rings draining meanwhile
+      if (e) return e;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(w->p_timeout_ms)) return PCCL_ERR_TIMEOUT;
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  };
+  const size_t max_frag = PCCL_MBOX_BYTES / 2;
+  size_t off = 0;
+  do {
+    const size_t len = std::min(bytes - off, max_frag);
+    const uint64_t need = 64 + ((len + 63) & ~(uint64_t)63);
+    size_t pos = pr.head_sent[dst] % PCCL_MBOX_BYTES;
+    if (pos + need > PCCL_MBOX_BYTES) {  // frames are contiguous: skip to the ring's start
+      const uint64_t rest = PCCL_MBOX_BYTES - pos;
+      s = wait_space(rest);
+      if (s) return s;
+      Frame k{kFrameMagic, 1, 0, 0, 0, 0, {0, 0}};
+      memcpy(pr.hdr, &k, 64);
+      CK(cudaMemcpyAsync(ring(w, dst, me) + pos, pr.hdr, 64, cudaMemcpyHostToDevice, pr.stream));
+      CK(cudaStreamSynchronize(pr.stream));
+      pr.head_sent[dst] += rest;
+      pos = 0;
+    }
+    s = wait_space(need);
+    if (s) return s;
+    Frame f{kFrameMagic, 0, tag, bytes, off, len, {0, 0}};
+    memcpy(pr.hdr, &f, 64);
+    CK(cudaMemcpyAsync(ring(w, dst, me) + pos, pr.hdr, 64, cudaMemcpyHostToDevice, pr.stream));
+    if (len) CK(cudaMemcpyAsync(ring(w, dst, me) + pos + 64, (const char *)buf + off, len, kind, pr.stream));
+    CK(cudaStreamSynchronize(pr.stream));  // frame complete in the receiver's memory before the head moves
+    pr.head_sent[dst] += need;
+    s = write_word(wctrl(w, dst, PCCL_WCTRL_HEAD + me), pr.head_sent[dst]);
+    if (s) return s;
+    off += len;
+  } while (off < bytes);
+  return PCCL_SUCCESS;
+}
+
+// Blocking receive of the first message from `src` with `tag`. buf == nullptr:
+// probe (wait until one is complete, report its size, leave it queued).
+int p2p_recv(pccl_world *w, int me, int src, int64_t tag, void *buf, size_t cap, bool host, size_t *bytes) {
+  int s = p2p_init(w, me);
+  if (s) return s;
+  P2PRank &pr = w->p2p[me];
+  const auto t0 = std::chrono::steady_clock::now();
+  while (true) {
+    auto &q = pr.unexpected[src];
+    for (auto it = q.begin(); it != q.end(); ++it) {
+      if (it->tag != tag) continue;
+      if (bytes) *bytes = it->bytes;
+      if (!buf) return PCCL_SUCCESS;
+      if (cap < it->bytes) return PCCL_ERR_LENGTH_MISMATCH;
+      if (it->bytes)
+        CK(cudaMemcpy(buf, it->dev, it->bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice));
+      cudaFree(it->dev);
+      q.erase(it);
+      return PCCL_SUCCESS;
+    }
+    if (src != me) {
+      s = p2p_progress(w, me);
+      if (s) return s;
+      bool got = false;
+      for (auto &m : q) got |= m.tag == tag;
+      if (got) continue;
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(w->p_timeout_ms)) return PCCL_ERR_TIMEOUT;
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// group ranks -> world ranks; `me` must be this process's rank in real mode
+int p2p_ranks(pccl_comm *c, int me, int peer, int *wme, int *wpeer) {
+  if (!c || me < 0 || me >= c->gs || peer < 0 || peer >= c->gs) return PCCL_ERR_INDEX_OUT_OF_RANGE;
+  if (!c->w->emu && me != c->gi) return PCCL_ERR_INVALID_ARGUMENT;
+  *wme = c->members[me];
+  *wpeer = c->members[peer];
+  CK(cudaSetDevice(c->w->device));
+  return check_world_err(c->w);
+}
+
+}  // namespace
+
+// ============================================================================
 // C ABI
 // ============================================================================
 extern "C" {
@@ -1508,6 +1721,13 @@ int pccl_world_destroy(pccl_world_t w) {
   cudaSetDevice(w->device);
   cudaDeviceSynchronize();
   for (auto &kv : w->comm_cache) delete kv.second;
+  for (auto &pr : w->p2p) {
+    for (auto &dq : pr.unexpected)
+      for (auto &m : dq) cudaFree(m.dev);
+    for (auto &m : pr.partial) cudaFree(m.dev);
+    if (pr.stream) cudaStreamDestroy(pr.stream);
+    if (pr.hdr) cudaFreeHost(pr.hdr);
+  }
   for (int i = 0; i < 4; ++i)
     if (w->nvls[i].used) pccl_nvls_destroy(w, i);
   for (int s = kMaxSegs - 1; s >= 0; --s)
@@ -1538,6 +1758,18 @@ int pccl_world_reset_flags(pccl_world_t w) {
   CK(cudaDeviceSynchronize());
   memset(w->epoch, 0, sizeof(w->epoch));
   memset(w->ce_calls, 0, sizeof(w->ce_calls));
+  for (auto &pr : w->p2p) {  // the mailbox counters were cleared with the arena
+    for (auto &dq : pr.unexpected) {
+      for (auto &m : dq) cudaFree(m.dev);
+      dq.clear();
+    }
+    for (int q = 0; q < PCCL_MAXR; ++q) {
+      cudaFree(pr.partial[q].dev);
+      pr.partial[q] = P2PMsg();
+      pr.in_partial[q] = false;
+      pr.head_sent[q] = pr.tail_read[q] = 0;
+    }
+  }
   for (int i = 0; i < 16; ++i) w->err_host[i] = 0;
   w->poisoned = 0;
   return PCCL_SUCCESS;
@@ -1901,6 +2133,21 @@ int pccl_comm_rank(pccl_comm_t c, int *rank) {
   if (!c || !rank) return PCCL_ERR_INVALID_ARGUMENT;
   *rank = c->gi;
   return PCCL_SUCCESS;
+}
+
+int pccl_send(pccl_comm_t c, int me, int dst, int64_t tag, const void *buf, size_t bytes, int host) {
+  int wme, wdst;
+  int s = p2p_ranks(c, me, dst, &wme, &wdst);
+  if (s) return s;
+  if (bytes && !buf) return PCCL_ERR_INVALID_ARGUMENT;
+  return p2p_send(c->w, wme, wdst, tag, buf, bytes, host != 0);
+}
+
+int pccl_recv(pccl_comm_t c, int me, int src, int64_t tag, void *buf, size_t cap, int host, size_t *bytes) {
+  int wme, wsrc;
+  int s = p2p_ranks(c, me, src, &wme, &wsrc);
+  if (s) return s;
+  return p2p_recv(c->w, wme, wsrc, tag, buf, cap, host != 0, bytes);
 }
 
 int pccl_all_gather(pccl_comm_t c, int algo, const void *send, void *recv, size_t count, int dtype, void *stream) {

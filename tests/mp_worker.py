@@ -377,6 +377,24 @@ def main() -> int:
     del a, b
     sync_point("registration")
 
+    # point-to-point over the mailbox rings (transport/base.py:140-152)
+    nxt, prv = (rank + 1) % p, (rank - 1) % p
+    big = np.full((5 << 20) // 4 + 3, rank + 0.5, np.float32)  # > one 2 MiB ring: fragments
+    got = comm.sendrecv(nxt, 21, big.tobytes()) if p == 2 else None
+    if p > 2:
+        comm.send(nxt, 21, big.tobytes())
+        got = comm.recv(prv, 21)
+    if np.frombuffer(got, np.float32)[0] != prv + 0.5 or len(got) != big.nbytes:
+        failures.append("p2p_big_ring")
+    for it in range(20):
+        comm.send(nxt, 100 + it, torch.full((4096,), float(rank * 1000 + it), device="cuda"))
+    for it in reversed(range(20)):  # out of tag order
+        t = torch.empty(4096, device="cuda")
+        comm.recv_into(prv, 100 + it, t)
+        if not bool((t == prv * 1000 + it).all()):
+            failures.append(f"p2p_tag_{it}")
+    sync_point("p2p")
+
     # online calibration: every rank must resolve "auto" identically afterwards
     from paper_2504_18658_b200 import selector, tuning
 
