@@ -481,7 +481,7 @@ def direct_reduce_scatter(comm, buf, *, order: str = "ring", out=None):
     return _run(comm, buf, True, "direct", order, out)
 
 
-def _resolve_auto(comm, collective: str, m_bytes: int) -> str:
+def _resolve_auto(comm, collective: str, m_bytes: int, order: str | None = None) -> str:
     """``auto``: the measured winner for (collective, p, size). Real mode
     first calibrates the live world when the table has nothing within 8x of
     this size at this GPU count (``tuning.autotune``, SPMD-uniform: the table
@@ -500,7 +500,7 @@ def _resolve_auto(comm, collective: str, m_bytes: int) -> str:
         m = max(16 * p * 4, m // (16 * p * 4) * (16 * p * 4))  # whole 16-byte units per rank, any dtype
         if not have or min(abs(math.log2(m / h)) for h in have) > 3:
             tuning.autotune(comm, collective, m, dtype=torch.float32 if collective == "all_gather" else torch.bfloat16)
-    return selector.choose_algorithm(collective, p, m_bytes)
+    return selector.choose_algorithm(collective, p, m_bytes, order)
 
 
 def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
@@ -514,8 +514,8 @@ def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
 
 def reduce_scatter(comm, buf, *, algorithm: str = "auto", order: str = "ring", out=None):
     """Dispatching reduce-scatter; ``auto`` picks from the measured selector."""
-    if algorithm == "auto":
-        algorithm = _resolve_auto(comm, "reduce_scatter", _nbytes(buf))
+    if algorithm == "auto":  # the data movement is measured; the fp32 add order is pinned by `order`
+        algorithm = _resolve_auto(comm, "reduce_scatter", _nbytes(buf), order)
     if algorithm not in REDUCE_SCATTER_ALGOS:
         raise Unsupported(f"unknown reduce-scatter algorithm {algorithm!r}")
     return _run(comm, buf, True, algorithm, order, out)

@@ -196,8 +196,9 @@ class FlatTable:
         self.entries.append(e)
         _choice_cache.clear()
 
-    def best(self, collective: str, p: int, m_bytes: float) -> str:
-        cands = [e for e in self.entries if e.collective == collective and e.p == p]
+    def best(self, collective: str, p: int, m_bytes: float, allowed=None) -> str:
+        cands = [e for e in self.entries if e.collective == collective and e.p == p
+                 and (allowed is None or e.algorithm in allowed)]
         if not cands:
             raise EmptyTable(f"no measurements for {collective} at p={p}")
         x = math.log(max(m_bytes, 1.0))
@@ -234,22 +235,35 @@ def flat_table() -> FlatTable | None:
 _choice_cache: dict = {}
 
 
-def choose_algorithm(collective: str, p: int, m_bytes: float) -> str:
-    """Measured winner for (collective, p, size); one-shot ``direct`` (the
-    fewest steps over a full-bandwidth switch) when nothing was measured.
-    Memoised per (collective, p, size); table edits clear the memo."""
-    key = (collective, p, m_bytes)
+def order_preserving(order: str) -> tuple:
+    """Reduce-scatter algorithms that add in ``order``: the one-shot direct
+    kernel folds in any order; ring adds in ring order and recursive halving
+    in butterfly order only. ``auto`` picks among these, so an fp32 result
+    never changes bits with the message size or the table."""
+    return {"ring": ("direct", "ring"), "recursive": ("direct", "recursive"), "rank": ("direct",)}[order]
+
+
+def choose_algorithm(collective: str, p: int, m_bytes: float, order: str | None = None) -> str:
+    """Measured winner for (collective, p, size) — for a reduce-scatter only
+    among the algorithms that reduce in ``order`` (default ring); one-shot
+    ``direct`` (the fewest steps over a full-bandwidth switch) when nothing
+    was measured. Memoised per (collective, p, size, order); table edits
+    clear the memo."""
+    if collective == "reduce_scatter" and order is None:
+        order = "ring"
+    key = (collective, p, m_bytes, order)
     hit = _choice_cache.get(key)
     if hit is None:
-        hit = _choice_cache[key] = _choose(collective, p, m_bytes)
+        hit = _choice_cache[key] = _choose(collective, p, m_bytes, order)
     return hit
 
 
-def _choose(collective: str, p: int, m_bytes: float) -> str:
+def _choose(collective: str, p: int, m_bytes: float, order: str | None) -> str:
     t = flat_table()
+    allowed = order_preserving(order) if collective == "reduce_scatter" else None
     if t is not None:
         try:
-            return t.best(collective, p, m_bytes)
+            return t.best(collective, p, m_bytes, allowed)
         except EmptyTable:
             pass
     return "direct"

@@ -248,3 +248,27 @@ def test_cost_params_defaults_and_formulas_match_reference():
     for N in (2, 3, 4, 8):
         for m in (1e3, 1e6, 1e9):
             assert choose_inter_algorithm(N, m, B200_NVLINK) == choose_inter_algorithm(N, m, P)
+
+
+def test_auto_reduce_scatter_keeps_the_requested_add_order():
+    """algorithm="auto" only picks among data movements that add in the
+    requested order (fp32 bits never depend on message size / table)."""
+    from paper_2504_18658_b200 import selector
+
+    t = FlatTable()
+    for m, (d, r, rec) in {1 << 20: (100, 50, 400), 1 << 27: (100, 300, 500)}.items():
+        t.add(FlatEntry("reduce_scatter", 4, m, "direct", d))
+        t.add(FlatEntry("reduce_scatter", 4, m, "ring", r))
+        t.add(FlatEntry("reduce_scatter", 4, m, "recursive", rec))
+    saved = selector._flat_table
+    selector._flat_table = t
+    selector._choice_cache.clear()
+    try:
+        assert selector.choose_algorithm("reduce_scatter", 4, 1 << 27) == "ring"
+        assert selector.choose_algorithm("reduce_scatter", 4, 1 << 20) == "direct"
+        assert selector.choose_algorithm("reduce_scatter", 4, 1 << 27, "recursive") == "recursive"
+        assert selector.choose_algorithm("reduce_scatter", 4, 1 << 27, "rank") == "direct"
+        assert selector.choose_algorithm("all_gather", 4, 1 << 27) == "direct"  # nothing measured: one-shot
+    finally:
+        selector._flat_table = saved
+        selector._choice_cache.clear()
