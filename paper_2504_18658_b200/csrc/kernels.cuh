@@ -1072,13 +1072,30 @@ __global__ void __launch_bounds__(kThreads) k_probe(char *local, const LaunchPar
         for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) st256(loc8 + i + u * nt, v[u]);
       }
     }
-  } else if (mode == 0) {
+  } else if (mode == 0 || mode == 6 || mode == 7) {  // 6 / 7: remote reductions (red.add f32x4 / bf16x8, sys scope)
     for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {
       uint4 v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) v[u] = __ldg(loc + i + u * nt);
+      if (mode == 0) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) rem[i + u * nt] = v[u];
+        for (int u = 0; u < kUnroll; ++u) if (i + u * nt < hi) rem[i + u * nt] = v[u];
+      } else if (mode == 6) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (i + u * nt < hi)
+            asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(rem + i + u * nt),
+                         "f"(__uint_as_float(v[u].x)), "f"(__uint_as_float(v[u].y)), "f"(__uint_as_float(v[u].z)),
+                         "f"(__uint_as_float(v[u].w))
+                         : "memory");
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (i + u * nt < hi)
+            asm volatile("red.relaxed.sys.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(rem + i + u * nt),
+                         "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                         : "memory");
+      }
     }
   } else {
     for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)kUnroll * nt) {

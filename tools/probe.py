@@ -29,7 +29,7 @@ def main():
     pats = {"uni": lambda r: (1 << 1) if r == 0 else 0, "bi": lambda r: (1 << (1 - r)) if r < 2 else 0,
             "a2a": lambda r: ((1 << p) - 1) & ~(1 << r), "ring": lambda r: 1 << ((r + 1) % p),
             "one2all": lambda r: (((1 << p) - 1) & ~1) if r == 0 else 0}
-    names = {0: "push16", 1: "pull16", 2: "push32", 3: "pull32", 4: "tma_push", 5: "tma_pull", 9: "ce_push"}
+    names = {0: "push16", 1: "pull16", 2: "push32", 3: "pull32", 4: "tma_push", 5: "tma_pull", 6: "red_f32x4", 7: "red_bf16x8", 9: "ce_push"}
     ap2 = os.environ.get("PROBE_TMA", "")  # "stages x tile", e.g. 4x32768
     if ap2:
         stg, tile = map(int, ap2.split("x"))
