@@ -45,6 +45,8 @@ class _SymmetricComm:
         self.comm = init_from_torch(group, staging_bytes=staging_bytes)  # collective over the group
         self.heap = self.comm.world.heap(heap_bytes)                      # collective
         self.algorithm = algorithm
+        self.calls = 0  # collectives issued through this object
+        self.bytes = 0  # all-gather output / reduce-scatter input bytes moved
 
     def allocate(self, size, *, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
         numel = math.prod(int(s) for s in size)
@@ -66,6 +68,8 @@ class PcclAllGather(_SymmetricComm, AllGather):
     def __call__(self, output_tensor: torch.Tensor, input_tensor: torch.Tensor, group: dist.ProcessGroup,
                  async_op: bool = False):
         all_gather_into_tensor(output_tensor.view(-1), input_tensor.view(-1), self.comm, algorithm=self.algorithm)
+        self.calls += 1
+        self.bytes += output_tensor.numel() * output_tensor.element_size()
         return None  # stream-ordered: FSDP records its event after this call
 
 
@@ -82,6 +86,8 @@ class PcclReduceScatter(_SymmetricComm, ReduceScatter):
             raise Unsupported(f"reduce-scatter op {op} (SUM / AVG only; FSDPModule."
                               "set_force_sum_reduction_for_comms(True) selects SUM)")
         reduce_scatter_tensor(output_tensor.view(-1), input_tensor.view(-1), self.comm, algorithm=self.algorithm)
+        self.calls += 1
+        self.bytes += input_tensor.numel() * input_tensor.element_size()
         if avg:
             output_tensor.div_(self.comm.size)
         return None

@@ -24,6 +24,7 @@ import torch.distributed as dist  # noqa: E402
 import torch.nn as nn  # noqa: E402
 
 H = int(os.environ.get("PCCL_FSDP_H", "4096"))
+REPS = 5
 
 
 class Block(nn.Module):
@@ -54,13 +55,17 @@ def build(dev):
     return model
 
 
-def step(model, x):
+def step(model, x, reps=1):
+    """Forward + backward; returns the last loss and the mean step time."""
     torch.cuda.synchronize()
+    dist.barrier()
     t0 = time.perf_counter()
-    loss = model(x).float().pow(2).mean()
-    loss.backward()
+    for _ in range(reps):
+        model.zero_grad(set_to_none=True)
+        loss = model(x).float().pow(2).mean()
+        loss.backward()
     torch.cuda.synchronize()
-    return loss.detach(), time.perf_counter() - t0
+    return loss.detach(), (time.perf_counter() - t0) / reps
 
 
 def full_params(model):
@@ -89,25 +94,23 @@ def main() -> int:
     failures = []
 
     ref = build(dev)
-    for _ in range(2):  # warm-up (allocator, cuBLAS handles)
-        ref.zero_grad(set_to_none=True)
-        step(ref, x)
-    ref.zero_grad(set_to_none=True)
-    loss_ref, t_ref = step(ref, x)
+    step(ref, x, 2)  # warm-up (allocator, cuBLAS handles)
+    _, t_ref = step(ref, x, REPS)
+    loss_ref, _ = step(ref, x)
     g_ref = grads(ref)
     w_ref = full_params(ref)
     del ref
     torch.cuda.empty_cache()
 
     ours = build(dev)
-    ag, rs = fsdp.install(ours, heap_bytes=3 << 30)
-    for _ in range(2):
-        ours.zero_grad(set_to_none=True)
-        step(ours, x)
+    ag, rs = fsdp.install(ours, heap_bytes=3 << 30, algorithm=os.environ.get("PCCL_FSDP_ALGO", "auto"))
+    step(ours, x, 2)
+    _, t = step(ours, x, REPS)
     ag.world.set_param("staged_bytes", 0)
     rs.world.set_param("staged_bytes", 0)
-    ours.zero_grad(set_to_none=True)
-    loss, t = step(ours, x)
+    calls0 = (ag.calls, rs.calls)
+    loss, _ = step(ours, x)
+    calls = (ag.calls - calls0[0], rs.calls - calls0[1])
     g_ours = grads(ours)
     w_ours = full_params(ours)
     ag.world.check()
@@ -132,9 +135,13 @@ def main() -> int:
             break
     if staged:
         failures.append(f"{staged} bytes went through staging")
+    if calls[0] < 2 or calls[1] != 2:  # >= one AG per layer (forward; again in backward after resharding), one RS
+        failures.append(f"B200 collectives issued per step (AG, RS) = {calls}")
+    diff = sum(int((a.view(torch.int16) != b.view(torch.int16)).sum()) for a, b in zip(g_ours, g_ref))
     n_params = sum(w.numel() for w in w_ours)
     msg = (f"[rank {rank}] params {n_params} (2 x 12h^2+13h, h={H}) step NCCL {t_ref * 1e3:.1f} ms, "
-           f"B200 {t * 1e3:.1f} ms, staged {staged} B, grad err/bound {worst:.3f}")
+           f"B200 {t * 1e3:.1f} ms, B200 collectives per step {calls}, staged {staged} B, grad err/bound {worst:.3f} "
+           f"({diff} elements differ from NCCL's)")
     print(msg + (" OK" if not failures else " FAIL " + "; ".join(failures)), flush=True)
     dist.barrier()
     return 1 if failures else 0
