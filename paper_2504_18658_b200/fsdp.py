@@ -37,14 +37,18 @@ from .communicator import init_from_torch
 from .errors import Unsupported
 
 DEFAULT_HEAP_BYTES = 4 << 30
+AG_CTAS = 32  # CTAs per collective inside FSDP (profiles/r2_fsdp2_p4.txt: 128 -> 32/64 cuts the step 6.8 -> 5.9 ms)
+RS_CTAS = 64
 
 
 class _SymmetricComm:
     def __init__(self, group=None, heap_bytes: int = DEFAULT_HEAP_BYTES, algorithm: str = "auto",
-                 staging_bytes: int = 64 << 20):
+                 staging_bytes: int = 64 << 20, ctas: int = 0):
         self.comm = init_from_torch(group, staging_bytes=staging_bytes)  # collective over the group
         self.heap = self.comm.world.heap(heap_bytes)                      # collective
         self.algorithm = algorithm
+        if ctas:  # CTAs per collective: FSDP overlaps the collectives with GEMMs competing for the SMs
+            self.comm.world.set_param("ctas", ctas)
         self.calls = 0  # collectives issued through this object
         self.bytes = 0  # all-gather output / reduce-scatter input bytes moved
 
@@ -93,15 +97,19 @@ class PcclReduceScatter(_SymmetricComm, ReduceScatter):
         return None
 
 
-def install(module, group=None, *, heap_bytes: int = DEFAULT_HEAP_BYTES, algorithm: str = "auto"):
+def install(module, group=None, *, heap_bytes: int = DEFAULT_HEAP_BYTES, algorithm: str = "auto",
+            ag_ctas: int = AG_CTAS, rs_ctas: int = RS_CTAS):
     """Route every FSDP2 module under ``module`` through the B200 collectives.
-    Collective over ``group`` (default: the world). Returns the
-    (all_gather, reduce_scatter) comm objects (their worlds' ``staged_bytes``
-    statistic shows whether any buffer had to be staged)."""
+    Collective over ``group`` (default: the world). ``ag_ctas`` / ``rs_ctas``:
+    CTAs per all-gather / reduce-scatter launch (0 = the library's automatic
+    choice, tuned for a collective running alone; FSDP overlaps them with the
+    GEMMs, which want the SMs). Returns the (all_gather, reduce_scatter) comm
+    objects (their worlds' ``staged_bytes`` statistic shows whether any
+    buffer had to be staged)."""
     from torch.distributed.fsdp import FSDPModule
 
-    ag = PcclAllGather(group, heap_bytes=heap_bytes, algorithm=algorithm)
-    rs = PcclReduceScatter(group, heap_bytes=heap_bytes, algorithm=algorithm)
+    ag = PcclAllGather(group, heap_bytes=heap_bytes, algorithm=algorithm, ctas=ag_ctas)
+    rs = PcclReduceScatter(group, heap_bytes=heap_bytes, algorithm=algorithm, ctas=rs_ctas)
     n = 0
     for m in module.modules():
         if isinstance(m, FSDPModule):

@@ -24,7 +24,7 @@ import torch.distributed as dist  # noqa: E402
 import torch.nn as nn  # noqa: E402
 
 H = int(os.environ.get("PCCL_FSDP_H", "4096"))
-REPS = 5
+REPS = int(os.environ.get("PCCL_FSDP_REPS", "5"))
 
 
 class Block(nn.Module):
@@ -103,7 +103,9 @@ def main() -> int:
     torch.cuda.empty_cache()
 
     ours = build(dev)
-    ag, rs = fsdp.install(ours, heap_bytes=3 << 30, algorithm=os.environ.get("PCCL_FSDP_ALGO", "auto"))
+    ag, rs = fsdp.install(ours, heap_bytes=3 << 30, algorithm=os.environ.get("PCCL_FSDP_ALGO", "auto"),
+                          ag_ctas=int(os.environ.get("PCCL_FSDP_AG_CTAS", fsdp.AG_CTAS)),
+                          rs_ctas=int(os.environ.get("PCCL_FSDP_RS_CTAS", fsdp.RS_CTAS)))
     step(ours, x, 2)
     _, t = step(ours, x, REPS)
     ag.world.set_param("staged_bytes", 0)
