@@ -557,12 +557,12 @@ def run_gpu(args):
         traffic = args.traffic
         if traffic is None and algo == "recursive" and args.dtype == "bf16" and args.size_mib == 128:
             # dram__bytes_read.sum + dram__bytes_write.sum of this launch, ncu --set full
-            # (profiles/r1_ncu_k_rs_rec_emulated.md): 1.878951 GB + 0.916030 GB
-            traffic = 2794981208
+            # (profiles/r2_ncu_k_rs_rec_emulated.md): 1.878912 GB + 0.916739 GB
+            traffic = 2795651328
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                 "algorithmic_bytes_per_launch": hbm, "traffic": traffic,
-                "traffic_source": "ncu --set full capture, profiles/r1_ncu_k_rs_rec_emulated.md" if traffic else None}
+                "traffic_source": "ncu --set full capture, profiles/r2_ncu_k_rs_rec_emulated.md" if traffic else None}
 
     cpu = None
     if rank == 0 and not real and not args.no_cpu:
