@@ -31,9 +31,10 @@
 #endif
 #define PCCL_MAX_CTAS 320
 #define PCCL_NSLOTS 256
-#define PCCL_CTRL_OFF (3 * PCCL_MAXR * PCCL_MAX_CTAS)
+#define PCCL_CTRL_OFF (4 * PCCL_MAXR * PCCL_MAX_CTAS)
 #define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter,
-                                              //   [2] work-item counter (direct kernels, see for_items)
+                                              //   [2] work-item counter (direct kernels, see for_items),
+                                              //   [3..10] per-step item counters (k_rs_rec_items)
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
 // After the slots: world-level control words, then the LL (low-latency)
 // message regions (see "LL protocol" below). Both live in segment 0, so every
@@ -58,7 +59,7 @@
 
 namespace pccl {
 
-enum FlagKind { F_READY = 0, F_DONE = 1, F_META = 2 };
+enum FlagKind { F_READY = 0, F_DONE = 1, F_META = 2, F_ITEM = 3 };  // F_ITEM: per-item progress (item kernels)
 enum Dt { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
 enum Algo { A_DIRECT = 0, A_RING = 1, A_REC = 2 };
 enum Order { O_RING = 0, O_REC = 1, O_RANK = 2 };
@@ -195,7 +196,7 @@ struct CtaEpilogue {
       const unsigned long long old = atomicAdd(ctrl + 1, 1ull);
       if (old == (unsigned long long)(c.P->ctas - 1)) {
         ctrl[1] = 0;
-        ctrl[2] = 0;  // work-item counter (every CTA's last claim returned before it got here)
+        for (int k = 2; k <= 10; ++k) ctrl[k] = 0;  // work-item counters (every CTA's last claim returned before it got here)
         *reinterpret_cast<volatile unsigned long long *>(ctrl) = c.epoch;
         if (c.ll_peers) {
           volatile uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
@@ -221,7 +222,7 @@ __device__ __noinline__ void abort_group(const Ctx &c, int code) {
     __threadfence_system();
   }
   const uint64_t v = PCCL_ABORT_BIT | (uint64_t)code;
-  const int per_member = 2 * PCCL_MAXR * PCCL_MAX_CTAS;  // READY + DONE
+  const int per_member = 4 * PCCL_MAXR * PCCL_MAX_CTAS;  // READY, DONE, META (copy-engine waits), ITEM
   for (int m = 0; m < c.gs; ++m) {
     uint64_t *slot = c.slot_in(m);
     for (int i = threadIdx.x; i < per_member; i += blockDim.x) st_relaxed_sys(slot + i, v);
@@ -522,9 +523,9 @@ __device__ __forceinline__ void cta_subslice(const Ctx &c, int t, int64_t &lo, i
 // (pull reads of the peers' inputs). Data pushed and consumed inside one
 // launch (RS direct push: push, then fold) keeps static slices.
 template <typename F>
-__device__ __forceinline__ void for_items(const Ctx &c, int64_t total, F &&body) {
+__device__ __forceinline__ void for_items(const Ctx &c, int64_t total, F &&body, int ctr_word = 2) {
   __shared__ long long s_item[2];
-  unsigned long long *ctr = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF + 2);
+  unsigned long long *ctr = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF + ctr_word);
   if (threadIdx.x == 0) s_item[0] = (long long)atomicAdd(ctr, 1ull);
   __syncthreads();
   long long cur = s_item[0];
@@ -535,6 +536,38 @@ __device__ __forceinline__ void for_items(const Ctx &c, int64_t total, F &&body)
     if (threadIdx.x == 0) s_item[k & 1] = (long long)nx;
     __syncthreads();
     cur = s_item[k & 1];
+  }
+}
+
+// Item-level progress (multi-step item kernels): member m's item i reached
+// `unit` — F_ITEM[m][i] in the reader's arena. CTA-wide wait; returns false
+// after aborting the group.
+__device__ __forceinline__ bool item_wait(Ctx &c, int m, int item, int unit) {
+  int code = 0;
+  if (threadIdx.x == 0) code = spin_ready(c, Ctx::word(c.my_slot, F_ITEM, m, item), unit);
+  if (!__syncthreads_and(code == 0)) {
+    __shared__ int s_code;
+    if (threadIdx.x == 0) s_code = code;
+    __syncthreads();
+    if (s_code != 0) abort_group(c, s_code);
+    return false;
+  }
+  return true;
+}
+// Publish item `item` at `unit` to member m and to myself (local dependency
+// of the next step), after a CTA barrier. The data is in my own memory (pull
+// kernels), so the local_fence publish applies (see cta_signal_local).
+__device__ __forceinline__ void item_signal(Ctx &c, int m, int item, int unit) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t v = ready_value(c, unit);
+    if (c.P->local_fence) {
+      fence_gpu();
+      st_relaxed_sys(Ctx::word(c.slot_in(m), F_ITEM, c.gi, item), v);
+    } else {
+      st_release_sys(Ctx::word(c.slot_in(m), F_ITEM, c.gi, item), v);
+    }
+    st_relaxed_sys(Ctx::word(c.my_slot, F_ITEM, c.gi, item), v);
   }
 }
 

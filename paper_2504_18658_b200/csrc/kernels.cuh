@@ -339,6 +339,63 @@ __global__ void __launch_bounds__(kThreads) k_rs_rec(const __grid_constant__ Lau
 }
 
 
+// RS recursive halving, pull, with per-step dynamic work items (rs_variant 7).
+// The static kernel above ties slice b to CTA b in every step, so a CTA whose
+// partner CTA was slow in step k waits at the boundary and the last CTAs form
+// a tail (profiles/r2_overhead_p4.md: boundary 3-5 us, tail 8 us at p=4).
+// Here every step's element range is cut into P.item-unit items claimed from
+// a per-step counter (CTRL[3 + k]); item i of step k waits for item i of
+// step k-1 on this rank (F_ITEM[gi][i], local) and on the partner
+// (F_ITEM[partner][i], remote), and publishes its own completion to the next
+// partner and to itself. Same arithmetic and order as k_rs_rec (butterfly,
+// wire rounding per step): bit-identical results. Exit: every CTA b signals
+// DONE to the partners and waits for theirs (a rank's kernel completes only
+// after all its CTAs, so the union over b covers every item).
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rs_rec_items(const __grid_constant__ LaunchParams P) {
+  using T = typename RUnit<DT, VEC>::T;
+  Ctx c = make_ctx(P);
+  CtaEpilogue fin(c);
+  const int gs = c.gs, L = ilog2(gs);
+  uint32_t partners = 0;
+  for (int k = 0; k < L; ++k) partners |= 1u << rechalf_partner(c.gi, gs, k);
+  const int p0 = rechalf_partner(c.gi, gs, 0);
+  cta_signal_entry(c, 1u << p0, 0);  // my send is ready (read by partner_0 in step 0)
+  if (!cta_wait(c, p0, 0)) return;    // partner_0's send is ready
+  char *sendp = P.send[c.r], *workp = P.work[c.r], *outp = P.out[c.r];
+  const int64_t I = P.item;
+  const int64_t nitems = (P.blk + I - 1) / I;
+  int lo_c = 0, hi_c = gs;
+  bool ok = true;
+  for (int k = 0; k < L && ok; ++k) {
+    const int half = (hi_c - lo_c) / 2, mid = lo_c + half;
+    const int partner = c.gi ^ half;
+    int m0, m1;
+    if (c.gi < mid) { m0 = lo_c; m1 = mid; } else { m0 = mid; m1 = hi_c; }
+    const bool last = (k == L - 1);
+    const int pw = c.world(partner);
+    const char *remote = (k == 0) ? P.send[pw] : P.work[pw];
+    const char *local = (k == 0) ? sendp : workp;
+    const int next = last ? -1 : rechalf_partner(c.gi, gs, k + 1);
+    for_items(c, nitems, [&](int64_t it) {
+      if (!ok) return;
+      if (k > 0 && (!item_wait(c, c.gi, (int)it, k) || !item_wait(c, partner, (int)it, k))) { ok = false; return; }
+      const int64_t lo = it * I, hi = lo + I < P.blk ? lo + I : P.blk;
+      for (int ch = m0; ch < m1; ++ch)
+        for (int j = 0; j < P.nsubblk; ++j) {
+          char *dst = last ? outp + (int64_t)j * P.out_sub_stride * (int64_t)sizeof(T) : rs_chunk<T>(P, workp, c.y, ch, j);
+          reduce2_units<DT, VEC, kUnroll>(dst, rs_chunk<T>(P, const_cast<char *>(local), c.y, ch, j),
+                                          rs_chunk<T>(P, const_cast<char *>(remote), c.y, ch, j), lo, hi);
+        }
+      if (!last) item_signal(c, next, (int)it, k + 1);
+    }, 3 + k);
+    lo_c = m0;
+    hi_c = m1;
+  }
+  if (!ok) return;
+  cta_exit(c, partners, partners);
+}
+
 // ============================================================================
 // PUSH family (ag_variant / rs_variant 1). Data moves as posted NVLink stores
 // into the consumer's symmetric buffer; the consumer only reads local HBM.

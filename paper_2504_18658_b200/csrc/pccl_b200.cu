@@ -95,7 +95,8 @@ struct pccl_world {
   int poisoned = 0;  // sticky device error
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
-  int64_t p_item_kib = 0;  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
+  int64_t p_item_kib = 0;
+  int64_t p_items_per_cta = 2;  // rs_variant 7: work items per CTA per step  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
@@ -249,7 +250,9 @@ KernelFn rs_direct_kernel(int order, int maxp) {
 template <int DT, bool VEC>
 KernelFn rs_kernel_dt(int algo, int order, int maxp, int variant) {
   if (algo == A_RING) return variant == 1 ? (KernelFn)k_rs_ring_push<DT, VEC> : (KernelFn)k_rs_ring<DT, VEC>;
-  if (algo == A_REC) return variant == 1 ? (KernelFn)k_rs_rec_push<DT, VEC> : (KernelFn)k_rs_rec<DT, VEC>;
+  if (algo == A_REC)
+    return variant == 1 ? (KernelFn)k_rs_rec_push<DT, VEC>
+                        : variant == 7 ? (KernelFn)k_rs_rec_items<DT, VEC> : (KernelFn)k_rs_rec<DT, VEC>;
   if (variant == 5) return rs_direct_pp_kernel<DT, VEC>(order, maxp);
   return variant == 1 ? rs_direct_kernel<DT, VEC, true>(order, maxp) : rs_direct_kernel<DT, VEC, false>(order, maxp);
 }
@@ -488,6 +491,11 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     ctas = std::max(1, std::min(ctas, cap / nrows));
   }
   P.ctas = ctas;
+  if (pl.variant == 7) {  // recursive halving with per-step work items: ~items_per_cta items per CTA
+    const int64_t target = std::min<int64_t>(PCCL_MAX_CTAS, std::max<int64_t>(1, w->p_items_per_cta * ctas));
+    const int64_t it = (P.blk + target - 1) / target;
+    P.item = std::max<int64_t>(32, (it + 31) / 32 * 32);
+  }
   if (w->p_trace) {
     // trace = K: the last K launches, one buffer each (K = 1: memset before
     // every launch; K > 1: consecutive launches run back to back, the ring is
@@ -1005,7 +1013,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
       const bool send_reg = resolve(w, ranks[0], sends[0], gs * chunk_bytes, &seg, &off);
       v = (!send_reg || algo == A_RING) ? 1 : 0;
     }
-    pl.variant = v == 1 ? 1 : (v == 5 && algo == A_DIRECT) ? 5 : 0;
+    pl.variant = v == 1 ? 1 : (v == 5 && algo == A_DIRECT) ? 5 : (v == 7 && algo == A_REC) ? 7 : 0;
   }
   Binder B{w, stream};
   for (size_t i = 0; i < ranks.size(); ++i) {
@@ -1801,6 +1809,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "trace")) return &w->p_trace;
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
   if (!strcmp(key, "staged_bytes")) return &w->p_staged_bytes;
+  if (!strcmp(key, "items_per_cta")) return &w->p_items_per_cta;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
   if (!strcmp(key, "item_kib")) return &w->p_item_kib;
@@ -1816,7 +1825,9 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
-  if (is_variant && value > 5) return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct)
+  if (is_variant && (value == 6 || value > 7 || (value == 7 && strcmp(key, "rs_variant"))))
+    return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items (RS recursive)
+  if (!strcmp(key, "items_per_cta") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;

@@ -97,7 +97,7 @@ def main() -> int:
         order = rng.choice(["ring", "rank"] + (["recursive"] if pow2 else []))
         kind = rng.choice(["sym", "plain", "misaligned", "host"] if coll != "hier" else ["sym", "plain", "misaligned"])
         w.set_param("item_kib", rng.choice([0, 0, 16, 64]))  # direct kernels: static slices / work items
-        w.set_param("rs_variant", rng.choice([-1, -1, 5]))  # 5: pipelined push (direct only; others fall back)
+        w.set_param("rs_variant", rng.choice([-1, -1, 5, 7]))  # 5: pipelined push (direct), 7: work items (recursive)
         # 5: copy engine (ring / recursive into a registered output; every rank
         # takes the same choice, a call that does not qualify is an error)
         use_ce = ce and coll == "ag" and kind == "sym" and algo != "direct" and rng.random() < 0.4

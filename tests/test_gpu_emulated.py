@@ -582,3 +582,37 @@ def test_world_empty_segments_are_released():
     gc.collect()
     w._run_pending()
     assert len(w._segments) <= before + 1
+
+
+@pytest.mark.parametrize("p", [2, 4, 8, 16])
+@pytest.mark.parametrize("items_per_cta", [1, 2, 4])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_rechalf_work_items_bit_exact(p, items_per_cta, dtype):
+    """rs_variant 7 (recursive halving with per-step dynamic work items):
+    bit-identical to the oracle's butterfly (fp32) / wire rounding (bf16)."""
+    pkg = _pkg()
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    w = emulated_world(p, 0)
+    rng = np.random.default_rng(p * 10 + items_per_cta)
+    n = 70001 * 8 // p * p // p + 5
+    ins32 = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    ins = [oracle.f32_to_bf16(x) for x in ins32] if dtype == "bf16" else ins32
+    want = oracle.rechalf_reduce_scatter(ins, dtype)
+    w.set_param("rs_variant", 7)
+    w.set_param("items_per_cta", items_per_cta)
+    w.set_param("ll_max", 0)
+    try:
+        for _ in range(2):
+            if dtype == "bf16":
+                outs = pkg.run_ranks(p, lambda c: pkg.rechalf_reduce_scatter(
+                    c, torch.from_numpy(ins[c.rank].view(np.int16)).view(torch.bfloat16).cuda())
+                    .view(torch.int16).cpu().numpy().view(np.uint16))
+            else:
+                outs = pkg.run_ranks(p, lambda c: pkg.rechalf_reduce_scatter(c, ins[c.rank]))
+            for r in range(p):
+                assert _bits_equal(outs[r], want[r]), r
+    finally:
+        w.set_param("rs_variant", -1)
+        w.set_param("items_per_cta", 2)
+        w.set_param("ll_max", -1)

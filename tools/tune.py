@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--variants", default="-1")
     ap.add_argument("--tma", default="4x32768", help="stages x tile bytes list, comma separated")
     ap.add_argument("--items", default="0", help="item_kib list (direct kernels; 0 = static CTA slices)")
+    ap.add_argument("--params", default="", help="key=value,... world params applied first")
     args = ap.parse_args()
     rank = int(os.environ["RANK"])
     p = int(os.environ["WORLD_SIZE"])
@@ -37,6 +38,9 @@ def main():
     L = _lib.lib()
     comm = pkg.init_from_torch(device=dev.index)
     world = comm.world
+    for kv in filter(None, args.params.split(",")):
+        k, v = kv.split("=")
+        world.set_param(k, int(v))
     S = args.size_mib << 20
     stream = torch.cuda.current_stream(dev)
     results = []
