@@ -1492,13 +1492,20 @@ int p2p_init(pccl_world *w, int me) {
   if (!pr.hdr) CK(cudaHostAlloc((void **)&pr.hdr, 64, cudaHostAllocDefault));
   return PCCL_SUCCESS;
 }
-uint64_t read_word(const uint64_t *dev) {
-  uint64_t v = 0;
-  cudaMemcpy(&v, dev, 8, cudaMemcpyDeviceToHost);
-  return v;
+// Control words and frames move on the rank's own non-blocking stream: a
+// mailbox operation never queues behind the collectives on the legacy
+// default stream (which may be waiting for the peer that waits for us).
+uint64_t read_word(P2PRank &pr, const uint64_t *dev) {
+  *(volatile uint64_t *)pr.hdr = 0;
+  if (cudaMemcpyAsync(pr.hdr, dev, 8, cudaMemcpyDeviceToHost, pr.stream) != cudaSuccess ||
+      cudaStreamSynchronize(pr.stream) != cudaSuccess)
+    return 0;
+  return *(volatile uint64_t *)pr.hdr;
 }
-int write_word(uint64_t *dev, uint64_t v) {
-  CK(cudaMemcpy(dev, &v, 8, cudaMemcpyHostToDevice));
+int write_word(P2PRank &pr, uint64_t *dev, uint64_t v) {
+  memcpy(pr.hdr, &v, 8);
+  CK(cudaMemcpyAsync(dev, pr.hdr, 8, cudaMemcpyHostToDevice, pr.stream));
+  CK(cudaStreamSynchronize(pr.stream));
   return PCCL_SUCCESS;
 }
 
@@ -1507,12 +1514,14 @@ int p2p_progress(pccl_world *w, int me) {
   P2PRank &pr = w->p2p[me];
   for (int src = 0; src < w->nranks; ++src) {
     if (src == me) continue;
-    const uint64_t head = read_word(wctrl(w, me, PCCL_WCTRL_HEAD + src));
+    const uint64_t head = read_word(pr, wctrl(w, me, PCCL_WCTRL_HEAD + src));
     const uint64_t start = pr.tail_read[src];
     while (pr.tail_read[src] < head) {
       const size_t pos = pr.tail_read[src] % PCCL_MBOX_BYTES;
       Frame f;
-      CK(cudaMemcpy(&f, ring(w, me, src) + pos, sizeof(f), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(pr.hdr, ring(w, me, src) + pos, sizeof(f), cudaMemcpyDeviceToHost, pr.stream));
+      CK(cudaStreamSynchronize(pr.stream));
+      memcpy(&f, pr.hdr, sizeof(f));
       if (f.magic != kFrameMagic) return PCCL_ERR_CUDA;  // corrupted ring: never expected
       if (f.kind == 1) {
         pr.tail_read[src] += PCCL_MBOX_BYTES - pos;
@@ -1523,10 +1532,13 @@ int p2p_progress(pccl_world *w, int me) {
         m = P2PMsg();
         m.tag = f.tag;
         m.bytes = f.total;
-        if (f.total) CK(cudaMalloc((void **)&m.dev, f.total));
+        if (f.total) CK(cudaMallocAsync((void **)&m.dev, f.total, pr.stream));  // stream-ordered: no device-wide sync
         pr.in_partial[src] = true;
       }
-      if (f.len) CK(cudaMemcpy(m.dev + f.off, ring(w, me, src) + pos + 64, f.len, cudaMemcpyDeviceToDevice));
+      if (f.len) {
+        CK(cudaMemcpyAsync(m.dev + f.off, ring(w, me, src) + pos + 64, f.len, cudaMemcpyDeviceToDevice, pr.stream));
+        CK(cudaStreamSynchronize(pr.stream));
+      }
       m.have += f.len;
       pr.tail_read[src] += 64 + ((f.len + 63) & ~(uint64_t)63);
       if (m.have == m.bytes) {
@@ -1536,7 +1548,7 @@ int p2p_progress(pccl_world *w, int me) {
       }
     }
     if (pr.tail_read[src] != start) {
-      const int s = write_word(wctrl(w, src, PCCL_WCTRL_TAIL + me), pr.tail_read[src]);
+      const int s = write_word(pr, wctrl(w, src, PCCL_WCTRL_TAIL + me), pr.tail_read[src]);
       if (s) return s;
     }
   }
@@ -1553,8 +1565,9 @@ int p2p_send(pccl_world *w, int me, int dst, int64_t tag, const void *buf, size_
     m.tag = tag;
     m.bytes = m.have = bytes;
     if (bytes) {
-      CK(cudaMalloc((void **)&m.dev, bytes));
-      CK(cudaMemcpy(m.dev, buf, bytes, kind));
+      CK(cudaMallocAsync((void **)&m.dev, bytes, pr.stream));
+      CK(cudaMemcpyAsync(m.dev, buf, bytes, kind, pr.stream));
+      CK(cudaStreamSynchronize(pr.stream));
     }
     pr.unexpected[me].push_back(m);
     return PCCL_SUCCESS;
@@ -1562,7 +1575,7 @@ int p2p_send(pccl_world *w, int me, int dst, int64_t tag, const void *buf, size_
   const auto t0 = std::chrono::steady_clock::now();
   auto wait_space = [&](uint64_t need) -> int {
     while (true) {
-      const uint64_t tail = read_word(wctrl(w, me, PCCL_WCTRL_TAIL + dst));
+      const uint64_t tail = read_word(pr, wctrl(w, me, PCCL_WCTRL_TAIL + dst));
       if (PCCL_MBOX_BYTES - (pr.head_sent[dst] - tail) >= need) return PCCL_SUCCESS;
       const int e = p2p_progress(w, me);  // keep my own rings draining meanwhile
       if (e) return e;
@@ -1595,7 +1608,7 @@ int p2p_send(pccl_world *w, int me, int dst, int64_t tag, const void *buf, size_
     if (len) CK(cudaMemcpyAsync(ring(w, dst, me) + pos + 64, (const char *)buf + off, len, kind, pr.stream));
     CK(cudaStreamSynchronize(pr.stream));  // frame complete in the receiver's memory before the head moves
     pr.head_sent[dst] += need;
-    s = write_word(wctrl(w, dst, PCCL_WCTRL_HEAD + me), pr.head_sent[dst]);
+    s = write_word(pr, wctrl(w, dst, PCCL_WCTRL_HEAD + me), pr.head_sent[dst]);
     if (s) return s;
     off += len;
   } while (off < bytes);
@@ -1616,9 +1629,12 @@ int p2p_recv(pccl_world *w, int me, int src, int64_t tag, void *buf, size_t cap,
       if (bytes) *bytes = it->bytes;
       if (!buf) return PCCL_SUCCESS;
       if (cap < it->bytes) return PCCL_ERR_LENGTH_MISMATCH;
-      if (it->bytes)
-        CK(cudaMemcpy(buf, it->dev, it->bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice));
-      cudaFree(it->dev);
+      if (it->bytes) {
+        CK(cudaMemcpyAsync(buf, it->dev, it->bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                           pr.stream));
+        CK(cudaStreamSynchronize(pr.stream));
+      }
+      if (it->dev) cudaFreeAsync(it->dev, pr.stream);  // cudaFree would synchronise the whole device
       q.erase(it);
       return PCCL_SUCCESS;
     }

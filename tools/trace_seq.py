@@ -26,11 +26,15 @@ def main():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--params", default="", help="key=value,... world params")
+    ap.add_argument("--backend", default="nccl", help="bootstrap process group (nccl | gloo)")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
     torch.cuda.set_device(dev)
-    dist.init_process_group("nccl", device_id=dev)
+    if a.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(a.backend)
     import paper_2504_18658_b200 as pkg
     from paper_2504_18658_b200 import _lib
 
