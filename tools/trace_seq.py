@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--params", default="", help="key=value,... world params")
     ap.add_argument("--backend", default="nccl", help="bootstrap process group (nccl | gloo)")
+    ap.add_argument("--poll", type=float, default=0, help="experiment: a host thread queries the stream every POLL ms (0 off)")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
@@ -71,6 +72,21 @@ def main():
         f()
     torch.cuda.synchronize()
     dist.barrier()
+    stop = None
+    if a.poll > 0:
+        import threading
+        import time as _t
+
+        stop = threading.Event()
+        qs = torch.cuda.Stream(dev)
+
+        def poller():
+            while not stop.is_set():
+                qs.query()
+                if a.poll >= 0.01:
+                    _t.sleep(a.poll / 1e3)
+
+        threading.Thread(target=poller, daemon=True).start()
     w.set_param("trace", K)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f()  # the trace ring is cleared before this launch
@@ -79,6 +95,8 @@ def main():
         f()
     e1.record(st)
     torch.cuda.synchronize()
+    if stop is not None:
+        stop.set()
     per_call = e0.elapsed_time(e1) * 1e3 / (K - 1)
     launches = [w.trace(back)[0] for back in range(K - 1, -1, -1)]  # oldest first
     w.set_param("trace", 0)
