@@ -56,8 +56,20 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);
+  if (P.item <= 0) {
+    // shift pattern with per-peer entry waits (see k_ag_direct_push)
+    for (int i = 1; i < c.gs; ++i) {
+      const int q = (c.gi + i) % c.gs;
+      if (!cta_wait(c, q, 0)) return;
+      const char *src = P.send[c.world(q)];
+      for (int t = 0; t < P.nsubblk; ++t)
+        copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t), src + (int64_t)t * P.send_sub_stride * U, lo, hi);
+    }
+    cta_exit(c, peers, peers);
+    return;
+  }
   if (!cta_wait_mask(c, peers, 0)) return;
-  if (P.item > 0) {
+  {
     // items (range j, sub-block t, source i), source fastest so that the
     // CTAs in flight spread over all peers
     const int nd = c.gs - 1;
@@ -70,13 +82,6 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct(const __grid_constant__ 
       copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t),
                              P.send[c.world(q)] + (int64_t)t * P.send_sub_stride * U, a, e);
     });
-  } else {
-    for (int i = 1; i < c.gs; ++i) {
-      const int q = (c.gi + i) % c.gs;  // rotate so every rank reads a different peer
-      const char *src = P.send[c.world(q)];
-      for (int t = 0; t < P.nsubblk; ++t)
-        copy_units<U, kUnroll>(ag_block<U>(P, P.recv[c.r], c.y, q, t), src + (int64_t)t * P.send_sub_stride * U, lo, hi);
-    }
   }
   cta_exit(c, peers, peers);
 }
@@ -175,8 +180,26 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
   cta_signal_entry(c, peers);  // my recv may be written
   int64_t lo, hi;
   split32(P.blk, P.ctas, c.b, lo, hi);
+  if (P.item <= 0) {
+    // Static slices, shift pattern: at step i every CTA of rank gi stores into
+    // peer gi + i (each GPU sends to one peer and receives from one at a
+    // time; a per-CTA rotation that spreads every GPU over all peers at once
+    // measured 1-3 % slower). Each peer is waited for just before the first
+    // store into it, not all of them up front.
+    for (int i = 1; i < c.gs; ++i) {
+      const int q = (c.gi + i) % c.gs;
+      if (!cta_wait(c, q, 0)) return;
+      char *dst = P.recv[c.world(q)];
+      for (int t = 0; t < P.nsubblk; ++t)
+        store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
+    }
+    cta_signal_mask(c, peers, 1);  // my block (this CTA's slice of it) has landed in your recv
+    if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
+    if (!cta_wait_mask(c, peers, 1)) return;
+    return;
+  }
   if (!cta_wait_mask(c, peers, 0)) return;
-  if (P.item > 0) {
+  {
     // items (range j, sub-block t, destination i), destination fastest
     const int nd = c.gs - 1;
     const int64_t nj = (P.blk + P.item - 1) / P.item;
@@ -188,13 +211,6 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
       store_units<U>(ag_block<U>(P, P.recv[c.world(q)], c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U,
                      a, e);
     });
-  } else {
-    for (int i = 1; i < c.gs; ++i) {
-      const int q = (c.gi + i) % c.gs;
-      char *dst = P.recv[c.world(q)];
-      for (int t = 0; t < P.nsubblk; ++t)
-        store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
-    }
   }
   cta_signal_mask(c, peers, 1);  // my block (this CTA's items of it) has landed in your recv
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
