@@ -81,3 +81,18 @@ def test_fsdp2_with_b200_collectives_matches_nccl():
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count(" OK") == n, out[-4000:]
+
+
+def test_torch_distributed_backend_matches_nccl():
+    """paper_2504_18658_b200.c10d: a "pccl" torch.distributed process group —
+    every supported collective bit-identical to NCCL's on the same inputs,
+    and FSDP1 on it matches FSDP1 on NCCL (tests/mp_c10d.py)."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    n = 4 if _ngpus() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29549", os.path.join(ROOT, "tests", "mp_c10d.py")]
+    r = subprocess.run(cmd, env=dict(os.environ, PCCL_TIMEOUT_MS="60000"), capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count("C10D OK") == n, out[-4000:]

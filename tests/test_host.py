@@ -272,3 +272,12 @@ def test_auto_reduce_scatter_keeps_the_requested_add_order():
     finally:
         selector._flat_table = saved
         selector._choice_cache.clear()
+
+
+def test_torch_distributed_backend_registers():
+    import torch.distributed as dist
+
+    from paper_2504_18658_b200 import c10d
+
+    assert c10d.BACKEND in dist.Backend.backend_list
+    assert issubclass(c10d.PcclProcessGroup, dist.ProcessGroup)
