@@ -80,6 +80,7 @@ struct LaunchParams {
   int tma_stages;   // TMA ring depth
   uint32_t tma_tile;  // TMA tile bytes
   int local_fence;  // 1: pull-kernel signals fence at gpu scope (data is in the writer's own HBM)
+  int wire;         // direct RS fold: round the partial to the storage type after every add (= step-wise algorithms)
   int64_t item;     // direct kernels: units per dynamically claimed work item (0: static CTA slices)
   int64_t timeout_ns;
   int64_t blk;              // units per sub-block

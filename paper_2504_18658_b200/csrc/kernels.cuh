@@ -630,9 +630,12 @@ __device__ __forceinline__ void copy_typed(T *d, const T *s, int64_t lo, int64_t
 
 // Fold the MAXP leaves src[i][off + e] of every element e in [lo, hi) in the
 // named order (registers only, fp32 accumulation) and store to dst[e].
+// wire = true: the partial is rounded to the storage type after every add, as
+// the step-wise kernels store it between steps (bit-identical to ring /
+// recursive halving in bf16 / fp16; a no-op for fp32).
 template <int DT, bool VEC, int ORDER, int MAXP>
 __device__ __forceinline__ void rs_fold(const typename RUnit<DT, VEC>::T *const *src, int gs, int64_t off,
-                                        typename RUnit<DT, VEC>::T *dst, int64_t lo, int64_t hi) {
+                                        typename RUnit<DT, VEC>::T *dst, int64_t lo, int64_t hi, bool wire = false) {
   using R = RUnit<DT, VEC>;
   using T = typename R::T;
   using Acc = typename R::Acc;
@@ -662,7 +665,10 @@ __device__ __forceinline__ void rs_fold(const typename RUnit<DT, VEC>::T *const 
         for (int h = MAXP / 2; h >= 1; h >>= 1) {
           if (h < gs) {  // levels above the group size do not exist (gs <= MAXP)
 #pragma unroll
-            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+            for (int m = 0; m < h; ++m) {
+              acc_add<Acc, R::N>(v[m], v[m ^ h]);
+              if (DT != DT_F32 && wire) v[m] = R::load(R::store(v[m]));
+            }
           }
         }
         acc = v[0];
@@ -676,7 +682,10 @@ __device__ __forceinline__ void rs_fold(const typename RUnit<DT, VEC>::T *const 
         acc = R::load(raw[0]);
 #pragma unroll
         for (int i = 1; i < MAXP; ++i)
-          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+          if (i < gs) {
+            acc_add<Acc, R::N>(acc, R::load(raw[i]));
+            if (DT != DT_F32 && wire) acc = R::load(R::store(acc));
+          }
       }
       dst[e] = R::store(acc);
     }
@@ -724,7 +733,8 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct(const __grid_constant__ 
   }
   auto fold = [&](int j, int64_t lo, int64_t hi) {
     rs_fold<DT, VEC, ORDER, MAXP>(src, gs, (int64_t)j * P.sub_stride,
-                                  reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride, lo, hi);
+                                  reinterpret_cast<T *>(P.out[c.r]) + (int64_t)j * P.out_sub_stride, lo, hi,
+                                  P.wire != 0);
   };
   if (!PUSH && P.item > 0) {  // pull: items (range, sub-block)
     const int64_t nj = (P.blk + P.item - 1) / P.item;
@@ -973,7 +983,10 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant
         acc = R::load(raw[0]);
 #pragma unroll
         for (int i = 1; i < MAXP; ++i)
-          if (i < gs) acc_add<Acc, R::N>(acc, R::load(raw[i]));
+          if (i < gs) {
+            acc_add<Acc, R::N>(acc, R::load(raw[i]));
+            if (DT != DT_F32 && P.wire) acc = R::load(R::store(acc));
+          }
       }
       dst[e] = R::store(acc);
     }

@@ -96,7 +96,8 @@ struct pccl_world {
   int64_t p_pdl = 1;          // programmatic dependent launch between back-to-back collectives
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   int64_t p_item_kib = 0;
-  int64_t p_items_per_cta = 2;  // rs_variant 7: work items per CTA per step  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
+  int64_t p_items_per_cta = 2;  // rs_variant 7: work items per CTA per step
+  int64_t p_hier_intra = -1;    // hierarchical intra phase: -1 auto (direct for M >= 3), 0 ring, 1 direct  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
@@ -316,6 +317,7 @@ struct Plan {
   char *send[PCCL_MAXR] = {}, *recv[PCCL_MAXR] = {}, *work[PCCL_MAXR] = {}, *out[PCCL_MAXR] = {};
   uint32_t place = 0;  // symmetric-placement hash (real mode)
   int variant = 0;
+  int wire = 0;        // direct RS: round after every add (step-wise rounding points)
 };
 
 int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
@@ -331,6 +333,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.nsub = (int)std::max<int64_t>(1, std::min<int64_t>(w->p_nsub, 32));
   P.variant = pl.variant;
   P.local_fence = (int)w->p_local_fence;
+  P.wire = pl.wire;
   P.tma_stages = (int)w->p_tma_stages;
   P.tma_tile = (uint32_t)w->p_tma_tile;
 
@@ -1132,11 +1135,16 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
       if (count) CK(cudaMemcpyAsync(outp[r] + (size_t)topo[r] * count * es, sends[i], count * es, cudaMemcpyDeviceToDevice, stream));
     }
   }
-  // phase 2: intra-node ring all-gather; member l's block = N sub-blocks at
-  // (n*M + l)*count
+  // phase 2: intra-node all-gather; member l's block = N sub-blocks at
+  // (n*M + l)*count. The reference's intra phase is a ring (hierarchy.py:171);
+  // an all-gather's output does not depend on the schedule, so for M >= 3 the
+  // one-step direct push replaces the M - 1 ring steps (param "hier_intra":
+  // -1 auto, 0 ring, 1 direct).
   if (M > 1) {
     Plan pl;
-    pl.coll = PCCL_ALL_GATHER; pl.algo = A_RING; pl.dtype = dtype; pl.count = (size_t)N * count; pl.gs = M;
+    const bool direct = w->p_hier_intra == 1 || (w->p_hier_intra < 0 && M >= 3);
+    pl.coll = PCCL_ALL_GATHER; pl.algo = direct ? A_DIRECT : A_RING; pl.dtype = dtype; pl.count = (size_t)N * count;
+    pl.gs = M;
     pl.nsubblk = N; pl.blk = (int64_t)count; pl.sub_stride = (int64_t)M * count; pl.istride = (int64_t)count;
     pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
     pl.variant = w->p_ag_variant == 0 ? 0 : 1;
@@ -1148,7 +1156,14 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
     }
-    for (int g = 0; g < N * M; ++g) { const int q = mem[g]; pl.recv[q] = outp[q]; pl.send[q] = outp[q]; }
+    for (int g = 0; g < N * M; ++g) {
+      const int q = mem[g];
+      pl.recv[q] = outp[q];
+      // ring forwards out of recv; direct reads my block (N sub-blocks at
+      // stride M * count, starting at local rank * count) as its send
+      pl.send[q] = direct ? outp[q] + (size_t)(g % M) * count * es : outp[q];
+    }
+    if (direct) pl.send_sub_stride = (int64_t)M * count;
     int s = launch(w, pl, stream);
     if (s) return s;
   }
@@ -1179,10 +1194,18 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
       return B.status;
   }
   const uint32_t place = w->emu ? 0 : B.place;
-  // phase 1: intra ring reduce-scatter; chunk l = N sub-blocks {nd*M + l}
+  // phase 1: intra reduce-scatter; chunk l = N sub-blocks {nd*M + l}. The
+  // reference's ring (hierarchy.py:193) fixes the add order (left fold from
+  // l+1) and, in bf16 / fp16, a rounding after every add; for M >= 3 the
+  // one-step direct kernel folds in exactly that order with the same rounding
+  // points (wire) — bit-identical, M - 2 fewer steps (param "hier_intra").
   if (M > 1) {
     Plan pl;
-    pl.coll = PCCL_REDUCE_SCATTER; pl.algo = A_RING; pl.dtype = dtype; pl.count = (size_t)N * n; pl.gs = M;
+    const bool direct = w->p_hier_intra == 1 || (w->p_hier_intra < 0 && M >= 3);
+    pl.coll = PCCL_REDUCE_SCATTER; pl.algo = direct ? A_DIRECT : A_RING; pl.dtype = dtype; pl.count = (size_t)N * n;
+    pl.gs = M;
+    pl.order = O_RING;
+    pl.wire = 1;
     pl.nsubblk = N; pl.blk = (int64_t)n; pl.sub_stride = (int64_t)M * n; pl.istride = (int64_t)n;
     pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
@@ -1193,7 +1216,9 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
       if (!g) return PCCL_ERR_CUDA;
       pl.rows.push_back({r, g});
     }
-    pl.variant = w->p_rs_variant == 1 ? 1 : 0;  // pull by default (measured faster here); push: staging = work
+    // pull by default (measured faster here); push: staging = work. The direct
+    // intra phase is the pull kernel (its push variant has no sub-block layout).
+    pl.variant = (!direct && w->p_rs_variant == 1) ? 1 : 0;
     for (int q : mem) {
       pl.send[q] = sendp[q];
       pl.work[q] = work[q];
@@ -1826,6 +1851,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "local_fence")) return &w->p_local_fence;
   if (!strcmp(key, "staged_bytes")) return &w->p_staged_bytes;
   if (!strcmp(key, "items_per_cta")) return &w->p_items_per_cta;
+  if (!strcmp(key, "hier_intra")) return &w->p_hier_intra;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
   if (!strcmp(key, "item_kib")) return &w->p_item_kib;
@@ -1836,7 +1862,7 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!w || !key) return PCCL_ERR_INVALID_ARGUMENT;
   int64_t *ref = param_ref(w, key);
   const bool is_variant = !strcmp(key, "ag_variant") || !strcmp(key, "rs_variant");
-  const bool auto_ok = is_variant || !strcmp(key, "ll_max");  // -1 = automatic
+  const bool auto_ok = is_variant || !strcmp(key, "ll_max") || !strcmp(key, "hier_intra");  // -1 = automatic
   if (!ref || value < (auto_ok ? -1 : 0)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
@@ -1844,6 +1870,7 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (is_variant && (value == 6 || value > 7 || (value == 7 && strcmp(key, "rs_variant"))))
     return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items (RS recursive)
   if (!strcmp(key, "items_per_cta") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "hier_intra") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;

@@ -616,3 +616,46 @@ def test_rechalf_work_items_bit_exact(p, items_per_cta, dtype):
         w.set_param("rs_variant", -1)
         w.set_param("items_per_cta", 2)
         w.set_param("ll_max", -1)
+
+
+@pytest.mark.parametrize("grid", [(2, 4), (4, 2), (2, 8), (1, 4), (4, 4)])
+@pytest.mark.parametrize("intra", [-1, 0, 1])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_hierarchical_intra_direct_is_bit_identical(grid, intra, dtype):
+    """The intra phase as the one-step direct kernel (param hier_intra, auto
+    for M >= 3): ring add order and, in bf16, the ring's per-step rounding —
+    bit-identical to the oracle's hier_reduce_scatter / hier_all_gather."""
+    pkg = _pkg()
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    N, M = grid
+    p = N * M
+    w = emulated_world(p, 0)
+    rng = np.random.default_rng(p + 10 * intra + (dtype == "bf16"))
+    n = 777
+    rs32 = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    ag32 = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+    rs = [oracle.f32_to_bf16(x) for x in rs32] if dtype == "bf16" else rs32
+    ag = [oracle.f32_to_bf16(x) for x in ag32] if dtype == "bf16" else ag32
+
+    def dev(x):
+        return torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda() if dtype == "bf16" else \
+            torch.from_numpy(x).cuda()
+
+    def host(t):
+        return t.view(torch.int16).cpu().numpy().view(np.uint16) if dtype == "bf16" else t.cpu().numpy()
+
+    w.set_param("hier_intra", intra)
+    try:
+        for inter in ["ring"] + (["recursive"] if N & (N - 1) == 0 else []):
+            plan = pkg.HierPlan(topo=pkg.Topology(N, M), inter_alg=inter)
+            got = pkg.run_ranks(p, lambda c: host(pkg.hier_reduce_scatter(plan, c, dev(rs[c.rank]))))
+            want = oracle.hier_reduce_scatter(rs, N, M, inter, dtype)
+            for r in range(p):
+                assert _bits_equal(got[r], want[r]), ("rs", inter, r)
+            got = pkg.run_ranks(p, lambda c: host(pkg.hier_all_gather(plan, c, dev(ag[c.rank]))))
+            want = oracle.hier_all_gather(ag, N, M, inter)
+            for r in range(p):
+                assert _bits_equal(got[r], want[r]), ("ag", inter, r)
+    finally:
+        w.set_param("hier_intra", -1)

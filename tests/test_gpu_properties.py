@@ -406,7 +406,7 @@ def test_param_validation():
     pkg = _pkg()
     w = pkg.emulated_world(2)
     cases = [("ll_max", [-1, 0, 8, 1 << 20], [-2]), ("ag_variant", [-1, 0, 1, 2, 3, 4, 5], [-2, 6, 7]),
-             ("rs_variant", [-1, 0, 1, 4, 5, 7], [6, 8]), ("items_per_cta", [1, 16], [0, 17]), ("ctas", [0, 1, 320], [-1, 321]), ("nsub", [1, 32], [0, 33]),
+             ("rs_variant", [-1, 0, 1, 4, 5, 7], [6, 8]), ("items_per_cta", [1, 16], [0, 17]), ("hier_intra", [-1, 0, 1], [-2, 2]), ("ctas", [0, 1, 320], [-1, 321]), ("nsub", [1, 32], [0, 33]),
              ("threads", [64, 512], [32, 100, 1024]), ("timeout_ms", [1, 20000], [0]), ("pdl", [0, 1], [-1]),
              ("local_fence", [0, 1], [-1]), ("item_kib", [0, 16, 64], [-1])]
     for key, good, bad in cases:
