@@ -631,7 +631,7 @@ def test_hierarchical_intra_direct_is_bit_identical(grid, intra, dtype):
     N, M = grid
     p = N * M
     w = emulated_world(p, 0)
-    rng = np.random.default_rng(p + 10 * intra + (dtype == "bf16"))
+    rng = np.random.default_rng(p + 10 * (intra + 1) + (dtype == "bf16"))
     n = 777
     rs32 = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
     ag32 = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
