@@ -249,10 +249,11 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
     # default data movement for symmetric buffers: AG push; RS ring push,
     # recursive / direct pull. Waits per CTA = the algorithm's steps plus the
     # push handshakes ("your buffer is free" before the first store, and the
-    # final arrival of the last forwarded block for AG).
+    # final arrival of the last forwarded block for AG; direct AG waits for
+    # each peer's "free" separately, just before its stores into that peer).
     L = steps
     expect = {("rs", "ring"): L + 1, ("rs", "recursive"): L, ("rs", "direct"): L,
-              ("ag", "ring"): L + 1, ("ag", "recursive"): 2 * L, ("ag", "direct"): L + 1}[(coll, algo)]
+              ("ag", "ring"): L + 1, ("ag", "recursive"): 2 * L, ("ag", "direct"): p}[(coll, algo)]
     for row in tr:
         for ev in row:
             kinds = [k for _, k, _ in ev if k not in (5, 6)]  # (5 CTA exit, 6 resident: timing only)
