@@ -77,7 +77,10 @@ typedef enum {
 typedef enum {
   PCCL_ORDER_RING = 0,      /* ((x_{c+1} + x_{c+2}) + ...) + x_c   (collectives.py:98-103)  */
   PCCL_ORDER_RECURSIVE = 1, /* recursive-halving butterfly          (collectives.py:150-164) */
-  PCCL_ORDER_RANK = 2       /* rank order from zeros                 (bench/oracles.py:12-19) */
+  PCCL_ORDER_RANK = 2,      /* rank order from zeros                 (bench/oracles.py:12-19) */
+  PCCL_ORDER_WIRE = 16      /* flag, direct only: round the partial to the storage type after every
+                               add, where ring / recursive halving store theirs (bit-identical to
+                               them in bf16 / fp16; fp32 is unaffected) */
 } pccl_order_t;
 
 typedef enum { PCCL_ALL_GATHER = 0, PCCL_REDUCE_SCATTER = 1 } pccl_collective_t;

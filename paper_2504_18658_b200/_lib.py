@@ -18,7 +18,10 @@ MAX_RANKS = 16
 # pccl_dtype_t / pccl_algo_t / pccl_order_t
 DTYPES = {"f32": 0, "bf16": 1, "f16": 2, "u8": 3, "i32": 4, "i64": 5, "f64": 6}
 ALGOS = {"direct": 0, "ring": 1, "recursive": 2}
-ORDERS = {"ring": 0, "recursive": 1, "rank": 2}
+ORDERS = {"ring": 0, "recursive": 1, "rank": 2,
+          # direct only: the partial is rounded after every add, where the
+          # step-wise algorithm of that name stores it (PCCL_ORDER_WIRE)
+          "ring/wire": 16, "recursive/wire": 17}
 ALL_GATHER, REDUCE_SCATTER = 0, 1
 
 _lib = None

@@ -349,7 +349,7 @@ def _fast_device(comm, buf, reduce: bool, algo: str, order: str, out):
     if reduce:
         if n % p:
             raise NotDivisible(f"input of {n} elements not divisible by p={p}")
-        if (algo == "recursive" or (algo == "direct" and order == "recursive")) and not pow2:
+        if (algo == "recursive" or (algo == "direct" and order.startswith("recursive"))) and not pow2:
             raise NonPowerOfTwo(f"recursive algorithms require power-of-two ranks, got {p}")
         cnt = n // p
         out_numel = cnt
@@ -396,7 +396,7 @@ def _run(comm, buf, reduce: bool, algo: str, order: str, out=None):
             raise NotDivisible(f"input of {arg.t.numel()} elements not divisible by p={p}")
         if algo == "recursive" and not is_power_of_two(p):
             raise NonPowerOfTwo(f"recursive halving requires power-of-two ranks, got {p}")
-        if algo == "direct" and order == "recursive" and not is_power_of_two(p):
+        if algo == "direct" and order.startswith("recursive") and not is_power_of_two(p):
             raise NonPowerOfTwo(f"recursive order requires power-of-two ranks, got {p}")
     elif algo == "recursive" and not is_power_of_two(p):
         raise NonPowerOfTwo(f"recursive doubling requires power-of-two ranks, got {p}")
@@ -475,7 +475,10 @@ def rechalf_reduce_scatter(comm, buf, *, out=None):
 def direct_reduce_scatter(comm, buf, *, order: str = "ring", out=None):
     """One-shot reduce-scatter: chunk r pulled from every peer and folded in
     fp32 in ``order`` ("ring" | "recursive" | "rank"), which makes fp32 results
-    bit-identical to the named step-wise algorithm."""
+    bit-identical to the named step-wise algorithm; bf16 / fp16 are rounded
+    once. "ring/wire" / "recursive/wire" also round after every add, where the
+    step-wise algorithm stores its partials: bit-identical to it for every
+    dtype (what ``reduce_scatter(algorithm="auto")`` uses)."""
     if order not in _lib.ORDERS:
         raise ValueError(f"unknown order {order!r}")
     return _run(comm, buf, True, "direct", order, out)
@@ -514,8 +517,13 @@ def all_gather(comm, buf, *, algorithm: str = "auto", out=None):
 
 def reduce_scatter(comm, buf, *, algorithm: str = "auto", order: str = "ring", out=None):
     """Dispatching reduce-scatter; ``auto`` picks from the measured selector."""
-    if algorithm == "auto":  # the data movement is measured; the fp32 add order is pinned by `order`
+    if algorithm == "auto":  # the data movement is measured; the add order is pinned by `order`
         algorithm = _resolve_auto(comm, "reduce_scatter", _nbytes(buf), order)
+        if algorithm == "direct" and order in ("ring", "recursive"):
+            # and so are the rounding points: the one-step kernel rounds where
+            # the step-wise algorithm would, so auto's result never depends on
+            # which data movement won (bit-identical for every dtype)
+            order = order + "/wire"
     if algorithm not in REDUCE_SCATTER_ALGOS:
         raise Unsupported(f"unknown reduce-scatter algorithm {algorithm!r}")
     return _run(comm, buf, True, algorithm, order, out)

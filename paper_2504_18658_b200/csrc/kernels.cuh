@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_pp(const __grid_constant
     if (!cta_wait_mask(c, peers, t + 1, b)) return;
     int64_t a, e;
     split32(hi - lo, nsub, t, a, e);
-    rs_fold<DT, VEC, ORDER, MAXP>(src, gs, 0, dst, lo + a, lo + e);
+    rs_fold<DT, VEC, ORDER, MAXP>(src, gs, 0, dst, lo + a, lo + e, P.wire != 0);
   }
 }
 
@@ -969,7 +969,10 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant
         for (int h = MAXP / 2; h >= 1; h >>= 1) {
           if (h < gs) {
 #pragma unroll
-            for (int m = 0; m < h; ++m) acc_add<Acc, R::N>(v[m], v[m ^ h]);
+            for (int m = 0; m < h; ++m) {
+              acc_add<Acc, R::N>(v[m], v[m ^ h]);
+              if (DT != DT_F32 && P.wire) v[m] = R::load(R::store(v[m]));
+            }
           }
         }
         acc = v[0];

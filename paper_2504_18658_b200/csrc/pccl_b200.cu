@@ -447,7 +447,8 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     P.base[y] = units(pl.base[rw.rank]);
     P.slot_off[y] = (uint32_t)((size_t)g->slot * PCCL_SLOT_WORDS);
     P.epoch[y] = 0;  // device-side (CTRL word of the slot), see make_ctx
-    P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order, pl.count, pl.dtype, pl.gs) ^ (pl.place * 2654435761u) ^
+    P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order | (pl.wire << 4), pl.count, pl.dtype, pl.gs) ^
+                 (pl.place * 2654435761u) ^
                  w->meta_skew[rw.rank]) & 0x7fffffffu;
   }
   for (int q = 0; q < w->nranks; ++q) {
@@ -958,6 +959,10 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
                       void *const *recvs, size_t recvcount, int dtype, cudaStream_t stream) {
   pccl_world *w = c->w;
   if (dtype != PCCL_FLOAT32 && dtype != PCCL_BFLOAT16 && dtype != PCCL_FLOAT16) return PCCL_ERR_UNSUPPORTED;
+  // order | PCCL_ORDER_WIRE (direct only): round the partial after every add,
+  // exactly where ring / recursive halving store theirs
+  const int wire = (order & PCCL_ORDER_WIRE) ? 1 : 0;
+  order &= ~PCCL_ORDER_WIRE;
   if (algo < 0 || algo > 2 || order < 0 || order > 2) return PCCL_ERR_INVALID_ARGUMENT;
   const int gs = c->gs;
   if (algo == A_REC && !is_pow2(gs)) return PCCL_ERR_NON_POWER_OF_TWO;
@@ -975,6 +980,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.coll = PCCL_REDUCE_SCATTER;
   pl.algo = algo;
   pl.order = algo == A_DIRECT ? order : 0;
+  pl.wire = algo == A_DIRECT ? wire : 0;
   pl.dtype = dtype;
   pl.count = recvcount;
   pl.gs = gs;

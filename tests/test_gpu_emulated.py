@@ -659,3 +659,31 @@ def test_hierarchical_intra_direct_is_bit_identical(grid, intra, dtype):
                 assert _bits_equal(got[r], want[r]), ("ag", inter, r)
     finally:
         w.set_param("hier_intra", -1)
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("n", [40, 70001])  # LL protocol / flag protocol
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("order", ["ring", "recursive"])
+def test_direct_wire_rounding_equals_stepwise(p, n, dtype, order):
+    """order "<name>/wire": the one-step direct kernel rounds where the
+    step-wise algorithm does — bit-identical to ring / recursive halving."""
+    pkg = _pkg()
+    rng = np.random.default_rng(p * n)
+    x32 = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    if dtype == "bf16":
+        ins = [oracle.f32_to_bf16(x) for x in x32]
+        dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()  # noqa: E731
+        host = lambda t: t.view(torch.int16).cpu().numpy().view(np.uint16)  # noqa: E731
+    else:
+        ins = [x.astype(np.float16) for x in x32]
+        dev = lambda x: torch.from_numpy(x).cuda()  # noqa: E731
+        host = lambda t: t.cpu().numpy()  # noqa: E731
+    want = (oracle.ring_reduce_scatter(ins, dtype) if order == "ring" else oracle.rechalf_reduce_scatter(ins, dtype))
+    got = pkg.run_ranks(p, lambda c: host(pkg.direct_reduce_scatter(c, dev(ins[c.rank]), order=order + "/wire")))
+    for r in range(p):
+        assert _bits_equal(got[r], want[r]), r
+    # auto never changes bits with the data movement it picks
+    got = pkg.run_ranks(p, lambda c: host(pkg.reduce_scatter(c, dev(ins[c.rank]), algorithm="auto", order=order)))
+    for r in range(p):
+        assert _bits_equal(got[r], want[r]), r
