@@ -281,3 +281,71 @@ def test_torch_distributed_backend_registers():
 
     assert c10d.BACKEND in dist.Backend.backend_list
     assert issubclass(c10d.PcclProcessGroup, dist.ProcessGroup)
+
+
+def test_symmetric_heap_allocator_is_deterministic_and_coalesces():
+    """The heap's first-fit allocator (no GPU: the segment is faked)."""
+    from paper_2504_18658_b200.world import SymmetricHeap
+
+    h = SymmetricHeap.__new__(SymmetricHeap)
+    h.nbytes = 1 << 20
+    h._free = [(0, h.nbytes)]
+    h._lock = threading.Lock()
+    a = h._alloc(1000)
+    b = h._alloc(1)
+    c = h._alloc(4096)
+    assert a == (0, 1024) and b == (1024, 256) and c == (1280, 4096)
+    h._release(*b)
+    assert h._alloc(200) == (1024, 256)  # first fit reuses the hole
+    h._release(1024, 256)
+    h._release(*a)
+    h._release(*c)
+    assert h._free == [(0, 1 << 20)]  # everything coalesced back
+    with pytest.raises(errors.OutOfMemory):
+        h._alloc(2 << 20)
+
+
+def test_auto_calibrates_uncovered_gpu_counts_once_per_size_bucket(monkeypatch):
+    """algorithm="auto" on a real communicator whose GPU count / size bucket
+    the table lacks runs tuning.autotune once (SPMD-uniform decision), then
+    uses the table; emulated communicators never calibrate."""
+    import torch
+
+    from paper_2504_18658_b200 import collectives as C
+    from paper_2504_18658_b200 import selector, tuning
+
+    calls = []
+
+    def fake_autotune(comm, collective, m, dtype=None):
+        calls.append((collective, m))
+        tuning._table().add(selector.FlatEntry(collective, comm.size, m, "ring", 100.0))
+        return {"ring": 100.0}
+
+    class FakeComm:
+        size, emulated = 6, False
+
+    def bucket(m_bytes, p=6):
+        m = 1 << max(20, min(28, (m_bytes - 1).bit_length()))
+        return m // (16 * p * 4) * (16 * p * 4)
+
+    saved = selector._flat_table
+    selector._flat_table = selector.FlatTable()
+    selector._choice_cache.clear()
+    monkeypatch.setattr(tuning, "autotune", fake_autotune)
+    monkeypatch.setattr(torch.cuda, "is_current_stream_capturing", lambda: False)
+    try:
+        assert C._resolve_auto(FakeComm(), "all_gather", 100 << 20) == "ring"
+        assert calls == [("all_gather", bucket(100 << 20))]
+        C._resolve_auto(FakeComm(), "all_gather", 50 << 20)    # within 8x of the measured bucket
+        C._resolve_auto(FakeComm(), "all_gather", 1 << 30)     # clamped to 256 MiB: within 8x
+        assert len(calls) == 1
+        C._resolve_auto(FakeComm(), "all_gather", 1 << 10)     # clamped to 1 MiB: 128x away
+        assert calls[-1] == ("all_gather", bucket(1 << 10)) and len(calls) == 2
+        C._resolve_auto(FakeComm(), "all_gather", 1 << 10)     # now measured
+        assert len(calls) == 2
+        FakeComm.emulated = True
+        C._resolve_auto(FakeComm(), "reduce_scatter", 1 << 20)
+        assert len(calls) == 2
+    finally:
+        selector._flat_table = saved
+        selector._choice_cache.clear()
