@@ -69,6 +69,7 @@ struct pccl_world {
   int device = 0;
   bool emu = false;
   Segment segs[kMaxSegs];
+  int seg_hi = 1;  // one past the highest segment index ever used (bounds the resolve() scan)
   int staging = -1;
   volatile int *err_host = nullptr;
   int *err_dev = nullptr;
@@ -169,7 +170,7 @@ int slot_for(pccl_world *w, uint32_t mask) {
 // Find (segment, offset) of a pointer owned by world rank r.
 bool resolve(pccl_world *w, int r, const void *p, size_t bytes, int *seg, size_t *off) {
   const char *c = (const char *)p;
-  for (int s = 1; s < kMaxSegs; ++s) {
+  for (int s = 1; s < w->seg_hi; ++s) {
     const Segment &S = w->segs[s];
     if (!S.used || !S.ptr[r]) continue;
     if (c >= S.ptr[r] && c + bytes <= S.ptr[r] + S.bytes) {
@@ -1934,6 +1935,7 @@ int pccl_segment_create(pccl_world_t w, size_t bytes, int *seg_id) {
     S.owned[w->rank] = true;
   }
   S.used = true;
+  w->seg_hi = std::max(w->seg_hi, s + 1);
   *seg_id = s;
   return PCCL_SUCCESS;
 }
@@ -1990,6 +1992,7 @@ int pccl_segment_register(pccl_world_t w, void *ptr, size_t bytes, int *seg_id) 
   S.reg = true;
   S.ptr[w->rank] = (char *)ptr;
   S.used = true;
+  w->seg_hi = std::max(w->seg_hi, s + 1);
   *seg_id = s;
   return PCCL_SUCCESS;
 }
@@ -2007,6 +2010,7 @@ int pccl_emu_segment_register(pccl_world_t w, void *const *ptrs, size_t bytes, i
     S.ptr[q] = (char *)ptrs[q];
   }
   S.used = true;
+  w->seg_hi = std::max(w->seg_hi, s + 1);
   *seg_id = s;
   return PCCL_SUCCESS;
 }
