@@ -81,6 +81,8 @@ struct LaunchParams {
   uint32_t tma_tile;  // TMA tile bytes
   int local_fence;  // 1: pull-kernel signals fence at gpu scope (data is in the writer's own HBM)
   int wire;         // direct RS fold: round the partial to the storage type after every add (= step-wise algorithms)
+  int chain;        // 1: first launch of a chained pair (publishes per-CTA completion), 2: second (waits for it
+                    //    instead of the PDL grid-completion wait); see "chained launches" below
   int64_t item;     // direct kernels: units per dynamically claimed work item (0: static CTA slices)
   int64_t timeout_ns;
   int64_t blk;              // units per sub-block
@@ -91,6 +93,7 @@ struct LaunchParams {
   int64_t base[PCCL_MAXR];  // per row: layout base offset (group-uniform)
   uint64_t epoch[PCCL_MAXR];
   uint32_t slot_off[PCCL_MAXR];  // per row: flag slot offset in words
+  uint32_t chain_slot_off[PCCL_MAXR];  // chain == 1, per row: slot of the second launch's group
   uint32_t meta[PCCL_MAXR];      // per row: call-signature hash
   int8_t row_rank[PCCL_MAXR];
   int8_t grank[PCCL_MAXR];
@@ -141,6 +144,7 @@ struct Ctx {
   uint64_t *tr;  // trace cursor base (nullptr: tracing off)
   int ntr;
   uint32_t ll_peers;  // LL kernels: world ranks whose channel counter the last CTA advances
+  uint64_t chain_epoch;  // chain == 1: the second launch's epoch (published per CTA at exit)
 
   __device__ __forceinline__ int world(int m) const { return P->gmem[y][m]; }
   __device__ __forceinline__ uint64_t *slot_in(int m) const {
@@ -157,9 +161,27 @@ struct Ctx {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Chained launches (hierarchical collectives, real mode): the two phases are
+// two launches on one stream with programmatic dependent launch. The second
+// does NOT wait for the first grid's completion (griddepcontrol.wait): its
+// CTA b waits only for CTA b of the first launch, which publishes, when it
+// exits, the second launch's epoch in the ITEM word [PCCL_MAXR - 1][b] of the
+// second group's slot in its own arena (st.release.gpu after a CTA barrier).
+// Both launches cut the element range into the same CTA slices (same grid,
+// same unit size: the host chains only 16-byte-aligned layouts), and the
+// second phase touches nothing of the first but that slice, so the phase
+// boundary costs no grid drain and no relaunch. The first launch's own
+// griddepcontrol.wait still orders the pair after everything before it.
+__device__ __forceinline__ uint64_t *chain_word(const LaunchParams &P, int r, uint32_t slot_off, int b) {
+  return P.flags[r] + slot_off + ((size_t)(F_ITEM * PCCL_MAXR + (PCCL_MAXR - 1)) * PCCL_MAX_CTAS + b);
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   const uint64_t t_resident = P.trace ? global_timer_ns() : 0;  // CTA scheduled (before the PDL wait)
-  pdl_wait();
+  if (P.chain != 2) pdl_wait();
   pdl_launch_dependents();
   Ctx c;
   c.P = &P;
@@ -177,6 +199,29 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
   c.ntr = 0;
   c.ll_peers = 0;
+  c.chain_epoch = 0;
+  if (P.chain == 1)
+    c.chain_epoch = *reinterpret_cast<volatile uint64_t *>(P.flags[c.r] + P.chain_slot_off[c.y] + PCCL_CTRL_OFF) + 1;
+  if (P.chain == 2) {  // wait for CTA b of the first launch (its slice of the first phase is complete)
+    __shared__ int s_chain;
+    if (threadIdx.x == 0) {
+      const uint64_t *w = chain_word(P, c.r, P.slot_off[c.y], c.b);
+      int code = 0;
+      uint32_t it = 0;
+      while (true) {
+        uint64_t v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+        if (v >= c.epoch) break;
+        if ((++it & 255u) == 0) {
+          if (*P.err != 0) { code = *P.err; break; }
+          if (global_timer_ns() - c.t0 > (uint64_t)P.timeout_ns) { code = 5; break; }  // PCCL_ERR_TIMEOUT
+        }
+      }
+      if (code && *P.err == 0) *P.err = code;  // the body's first wait then sees the world error
+      s_chain = code;
+    }
+    __syncthreads();
+  }
   if (c.tr && threadIdx.x == 0) {
     c.tr[c.ntr++] = (t_resident << 16) | (TR_RESIDENT << 12);
     c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
@@ -190,6 +235,11 @@ struct CtaEpilogue {
   Ctx &c;
   __device__ explicit CtaEpilogue(Ctx &cc) : c(cc) {}
   __device__ ~CtaEpilogue() {
+    if (c.P->chain == 1) {  // this CTA's slice of the first phase is complete: release the second launch's CTA b
+      __syncthreads();
+      if (threadIdx.x == 0 && *c.P->err == 0)
+        st_release_gpu(chain_word(*c.P, c.r, c.P->chain_slot_off[c.y], c.b), c.chain_epoch);
+    }
     if (c.tr && threadIdx.x == 0 && c.ntr < PCCL_TRACE_EVENTS)
       c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)TR_EXIT << 12);
     if (threadIdx.x == 0) {

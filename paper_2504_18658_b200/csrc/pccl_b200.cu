@@ -98,7 +98,8 @@ struct pccl_world {
   int64_t p_local_fence = 1;  // pull-kernel signals: gpu-scope fence + relaxed sys store (see device.cuh)
   int64_t p_item_kib = 0;
   int64_t p_items_per_cta = 2;  // rs_variant 7: work items per CTA per step
-  int64_t p_hier_intra = -1;    // hierarchical intra phase: -1 auto (direct for M >= 3), 0 ring, 1 direct  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
+  int64_t p_hier_intra = -1;    // hierarchical intra phase: -1 auto (direct for M >= 3), 0 ring, 1 direct
+  int64_t p_hier_chain = 1;     // hierarchical: chain the two phase launches (device.cuh "chained launches")  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
@@ -319,6 +320,9 @@ struct Plan {
   uint32_t place = 0;  // symmetric-placement hash (real mode)
   int variant = 0;
   int wire = 0;        // direct RS: round after every add (step-wise rounding points)
+  int chain = 0;       // chained pair (device.cuh): 1 first launch, 2 second launch
+  uint32_t chain_slot_off[PCCL_MAXR] = {};  // chain 1, per row: the second group's slot (words)
+  int force_ctas = 0;  // > 0: CTAs per row (chained launches must cut identical slices)
 };
 
 int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
@@ -335,6 +339,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.variant = pl.variant;
   P.local_fence = (int)w->p_local_fence;
   P.wire = pl.wire;
+  P.chain = pl.chain;
   P.tma_stages = (int)w->p_tma_stages;
   P.tma_tile = (uint32_t)w->p_tma_tile;
 
@@ -447,6 +452,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     P.grank[y] = (int8_t)gi;
     P.base[y] = units(pl.base[rw.rank]);
     P.slot_off[y] = (uint32_t)((size_t)g->slot * PCCL_SLOT_WORDS);
+    P.chain_slot_off[y] = pl.chain_slot_off[y];
     P.epoch[y] = 0;  // device-side (CTRL word of the slot), see make_ctx
     P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order | (pl.wire << 4), pl.count, pl.dtype, pl.gs) ^
                  (pl.place * 2654435761u) ^
@@ -462,7 +468,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
 
   // ---- grid
   const int threads = (int)std::max<int64_t>(64, std::min<int64_t>(w->p_threads, kThreads));
-  int ctas = (int)w->p_ctas;
+  int ctas = pl.force_ctas > 0 ? pl.force_ctas : (int)w->p_ctas;
   if (ctas <= 0) {
     // auto (measured, tools/sweep.py at p=2/4, profiles/r1_sweep_p*.csv):
     // latency-bound small messages want fewer CTAs (fewer flags); >= 16 MiB
@@ -494,6 +500,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     }
     const int cap = std::max(1, per_sm) * w->sms;
     ctas = std::max(1, std::min(ctas, cap / nrows));
+    if (pl.chain && ctas != pl.force_ctas) return PCCL_ERR_UNSUPPORTED;  // chained slices must match (host checks caps)
   }
   P.ctas = ctas;
   if (pl.variant == 7) {  // recursive halving with per-step work items: ~items_per_cta items per CTA
@@ -1114,10 +1121,30 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
     if (staged) copy_out.push_back({staged, (char *)recvs[i]});
   }
   const uint32_t place = w->emu ? 0 : B.place;
+  // Chain the two phases (device.cuh "chained launches") when both exist, the
+  // slices of both launches are identical (16-byte units everywhere, static
+  // slices, the same CTA count) and PDL is on.
+  bool chain = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
+               w->p_ctas <= 128 && (count * es) % 16 == 0;
+  for (size_t i = 0; chain && i < ranks.size(); ++i)
+    chain = ((uintptr_t)outp[ranks[i]] % 16 == 0) && ((uintptr_t)sends[i] % 16 == 0);
+  const int chain_ctas = w->p_ctas > 0 ? (int)w->p_ctas : 128;
   // phase 1: inter-node all-gather on every stride-M group, blocks land at
   // their global positions (g*count) directly (fused shuffle)
   if (N > 1) {
     Plan pl;
+    if (chain) {
+      pl.chain = 1;
+      pl.force_ctas = chain_ctas;
+      for (size_t i = 0; i < ranks.size(); ++i) {  // row i: the intra group of ranks[i] runs phase 2
+        const int nd = topo[ranks[i]] / M;
+        std::vector<int> grp;
+        for (int l = 0; l < M; ++l) grp.push_back(mem[nd * M + l]);
+        pccl_comm *g2 = cached_group(w, grp, 1 + M + nd);
+        if (!g2) return PCCL_ERR_CUDA;
+        pl.chain_slot_off[i] = (uint32_t)((size_t)g2->slot * PCCL_SLOT_WORDS);
+      }
+    }
     pl.coll = PCCL_ALL_GATHER; pl.algo = inter; pl.dtype = dtype; pl.count = count; pl.gs = N;
     pl.blk = (int64_t)count; pl.istride = (int64_t)M * count; pl.send_sub_stride = (int64_t)count;
     pl.local_copy = 1;
@@ -1152,6 +1179,10 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
     const bool direct = w->p_hier_intra == 1 || (w->p_hier_intra < 0 && M >= 3);
     pl.coll = PCCL_ALL_GATHER; pl.algo = direct ? A_DIRECT : A_RING; pl.dtype = dtype; pl.count = (size_t)N * count;
     pl.gs = M;
+    if (chain) {
+      pl.chain = 2;
+      pl.force_ctas = chain_ctas;
+    }
     pl.nsubblk = N; pl.blk = (int64_t)count; pl.sub_stride = (int64_t)M * count; pl.istride = (int64_t)count;
     pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
     pl.variant = w->p_ag_variant == 0 ? 0 : 1;
@@ -1201,6 +1232,12 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
       return B.status;
   }
   const uint32_t place = w->emu ? 0 : B.place;
+  // chained phases (see do_hier_all_gather)
+  bool chain = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
+               w->p_ctas <= 128 && (n * es) % 16 == 0 && w->p_rs_variant != 1;
+  for (size_t i = 0; chain && i < ranks.size(); ++i)
+    chain = ((uintptr_t)sendp[ranks[i]] % 16 == 0) && ((uintptr_t)recvs[i] % 16 == 0);
+  const int chain_ctas = w->p_ctas > 0 ? (int)w->p_ctas : 128;
   // phase 1: intra reduce-scatter; chunk l = N sub-blocks {nd*M + l}. The
   // reference's ring (hierarchy.py:193) fixes the add order (left fold from
   // l+1) and, in bf16 / fp16, a rounding after every add; for M >= 3 the
@@ -1213,6 +1250,18 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
     pl.gs = M;
     pl.order = O_RING;
     pl.wire = 1;
+    if (chain) {
+      pl.chain = 1;
+      pl.force_ctas = chain_ctas;
+      for (size_t i = 0; i < ranks.size(); ++i) {  // row i: the inter group of ranks[i] runs phase 2
+        const int j = topo[ranks[i]] % M;
+        std::vector<int> grp;
+        for (int nd = 0; nd < N; ++nd) grp.push_back(mem[nd * M + j]);
+        pccl_comm *g2 = cached_group(w, grp, 1 + j);
+        if (!g2) return PCCL_ERR_CUDA;
+        pl.chain_slot_off[i] = (uint32_t)((size_t)g2->slot * PCCL_SLOT_WORDS);
+      }
+    }
     pl.nsubblk = N; pl.blk = (int64_t)n; pl.sub_stride = (int64_t)M * n; pl.istride = (int64_t)n;
     pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
@@ -1244,6 +1293,10 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
   if (N > 1) {
     Plan pl;
     pl.coll = PCCL_REDUCE_SCATTER; pl.algo = inter; pl.dtype = dtype; pl.count = n; pl.gs = N;
+    if (chain) {
+      pl.chain = 2;
+      pl.force_ctas = chain_ctas;
+    }
     pl.blk = (int64_t)n; pl.istride = (int64_t)n; pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
       const int r = ranks[i], j = topo[r] % M;
@@ -1859,6 +1912,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "staged_bytes")) return &w->p_staged_bytes;
   if (!strcmp(key, "items_per_cta")) return &w->p_items_per_cta;
   if (!strcmp(key, "hier_intra")) return &w->p_hier_intra;
+  if (!strcmp(key, "hier_chain")) return &w->p_hier_chain;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
   if (!strcmp(key, "item_kib")) return &w->p_item_kib;
@@ -1878,6 +1932,7 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
     return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items (RS recursive)
   if (!strcmp(key, "items_per_cta") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "hier_intra") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;
+  if (!strcmp(key, "hier_chain") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_stages") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "tma_tile") && (value < 16 || value % 16 || value > 200 * 1024)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "timeout_ms") && value < 1) return PCCL_ERR_INVALID_ARGUMENT;

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--colls", default="ag_f32,rs_bf16")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--write-table", action="store_true")
+    ap.add_argument("--no-hier", action="store_true", help="skip the hierarchical N x M groupings (C4)")
     args = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
@@ -93,6 +94,19 @@ def main():
                     rows.append(dict(coll=coll, p=p, S=S, algo=algo, ctas=ctas, us=t * 1e6,
                                      busbw=S * (p - 1) / p / t / 1e9))
             w.set_param("ctas", 0)
+            # hierarchical virtual groupings (C4: N x M in {2x4, 4x2, 2x2}), auto CTAs
+            grids = [] if args.no_hier else [(N, p // N) for N in (2, 4) if p % N == 0 and 1 < N < p]
+            for N, M in grids:
+                for inter in ["ring"] + (["recursive"] if N & (N - 1) == 0 else []):
+                    ia = _lib.ALGOS[inter]
+                    w.ensure_staging(int(L.pccl_staging_bytes(0 if kind == "ag" else 1, 3, p, n, code)))
+                    hf = L.pccl_hier_all_gather if kind == "ag" else L.pccl_hier_reduce_scatter
+                    f = lambda: _lib.check(hf(w.handle, N, M, ia, big_in.data_ptr(), big_out.data_ptr(), n, code,  # noqa
+                                              stream.cuda_stream))
+                    t = timeit(f)
+                    w.check()
+                    rows.append(dict(coll=coll, p=p, S=S, algo=f"hier{N}x{M}_{inter}", ctas=0, us=t * 1e6,
+                                     busbw=S * (p - 1) / p / t / 1e9))
             if kind == "ag":
                 f = lambda: dist.all_gather_into_tensor(nout[: n * p], nin[:n])  # noqa
             else:
@@ -100,12 +114,14 @@ def main():
             t = timeit(f)
             rows.append(dict(coll=coll, p=p, S=S, algo="nccl", ctas=0, us=t * 1e6, busbw=S * (p - 1) / p / t / 1e9))
             if rank == 0:
-                best = max((r for r in rows if r["coll"] == coll and r["S"] == S and r["algo"] != "nccl"),
-                           key=lambda r: r["busbw"])
+                best = max((r for r in rows if r["coll"] == coll and r["S"] == S and r["algo"] != "nccl"
+                            and not r["algo"].startswith("hier")), key=lambda r: r["busbw"])
+                hier = [r for r in rows if r["coll"] == coll and r["S"] == S and r["algo"].startswith("hier")]
                 nc = rows[-1]
                 print(f"p={p} {coll:8s} S={S / 2**20:8.2f} MiB  best {best['algo']:9s} ctas={best['ctas']:3d} "
                       f"{best['busbw']:7.1f} GB/s ({best['us']:8.1f} us)   NCCL {nc['busbw']:7.1f} GB/s ({nc['us']:8.1f} us)"
-                      f"  ratio {best['busbw'] / nc['busbw']:.2f}", flush=True)
+                      f"  ratio {best['busbw'] / nc['busbw']:.2f}"
+                      + "".join(f"  {h['algo']} {h['busbw']:.1f}" for h in hier), flush=True)
     if rank == 0:
         os.makedirs("gpurun_out", exist_ok=True)
         with open(f"gpurun_out/sweep_p{p}.csv", "w", newline="") as fh:
