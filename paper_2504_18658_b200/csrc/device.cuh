@@ -54,6 +54,10 @@
 #define PCCL_MBOX_BYTES ((size_t)2 << 20)
 #define PCCL_WCTRL_HEAD 16
 #define PCCL_WCTRL_TAIL 32
+// WCTRL [48]: device-side mirror of the world error word. Spinning CTAs poll
+// it instead of the host-mapped error word: 128 CTAs reading host memory at
+// once stalled a kernel's exits by up to 120 us (profiles/r2_overhead_p4.md).
+#define PCCL_WCTRL_ERR 48
 #define PCCL_FLAG_BYTES (PCCL_MBOX_OFF + (size_t)PCCL_MAXR * PCCL_MBOX_BYTES)
 #define PCCL_ABORT_BIT (1ull << 63)
 
@@ -129,6 +133,10 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ volatile uint64_t *err_mirror(const LaunchParams &P, int r) {
+  return P.flags[r] + PCCL_WCTRL_OFF + PCCL_WCTRL_ERR;
 }
 
 struct Ctx {
@@ -212,12 +220,15 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
         uint64_t v;
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
         if (v >= c.epoch) break;
-        if ((++it & 255u) == 0) {
-          if (*P.err != 0) { code = *P.err; break; }
+        if ((++it & 4095u) == 0) {  // rare host-memory reads: the first phase usually takes tens of us
+          if (const uint64_t e = *err_mirror(P, c.r)) { code = (int)e; break; }
           if (global_timer_ns() - c.t0 > (uint64_t)P.timeout_ns) { code = 5; break; }  // PCCL_ERR_TIMEOUT
         }
       }
-      if (code && *P.err == 0) *P.err = code;  // the body's first wait then sees the world error
+      if (code) {  // the body's first wait then sees the error
+        *err_mirror(P, c.r) = (uint64_t)code;
+        if (*P.err == 0) *P.err = code;
+      }
       s_chain = code;
     }
     __syncthreads();
@@ -236,9 +247,11 @@ struct CtaEpilogue {
   __device__ explicit CtaEpilogue(Ctx &cc) : c(cc) {}
   __device__ ~CtaEpilogue() {
     if (c.P->chain == 1) {  // this CTA's slice of the first phase is complete: release the second launch's CTA b
+      // (no check of the host-mapped error word here: 128 CTAs reading host
+      // memory at once stalled the exits by up to 120 us; a failed first phase
+      // has set the error word, which the second phase's waits observe)
       __syncthreads();
-      if (threadIdx.x == 0 && *c.P->err == 0)
-        st_release_gpu(chain_word(*c.P, c.r, c.P->chain_slot_off[c.y], c.b), c.chain_epoch);
+      if (threadIdx.x == 0) st_release_gpu(chain_word(*c.P, c.r, c.P->chain_slot_off[c.y], c.b), c.chain_epoch);
     }
     if (c.tr && threadIdx.x == 0 && c.ntr < PCCL_TRACE_EVENTS)
       c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)TR_EXIT << 12);
@@ -268,10 +281,12 @@ __device__ __forceinline__ void trace_ev(Ctx &c, int kind, int unit) {
 // Flood ABORT into every member's slot (all sources, all CTAs) so that every
 // waiter of this group, on every GPU, wakes up. Called by a whole CTA.
 __device__ __noinline__ void abort_group(const Ctx &c, int code) {
-  if (threadIdx.x == 0 && *c.P->err == 0) {
-    *c.P->err = code;
+  if (threadIdx.x == 0 && *err_mirror(*c.P, c.r) == 0) {
+    *c.P->err = code;  // host-visible (the host reports it); written once per rank
     __threadfence_system();
   }
+  if (threadIdx.x < c.gs)  // every member's device mirror: its spinning CTAs stop without host-memory reads
+    st_relaxed_sys(const_cast<uint64_t *>(err_mirror(*c.P, c.world(threadIdx.x))), (uint64_t)code);
   const uint64_t v = PCCL_ABORT_BIT | (uint64_t)code;
   const int per_member = 4 * PCCL_MAXR * PCCL_MAX_CTAS;  // READY, DONE, META (copy-engine waits), ITEM
   for (int m = 0; m < c.gs; ++m) {
@@ -289,7 +304,7 @@ __device__ __forceinline__ int spin_ge(const Ctx &c, const uint64_t *w, uint64_t
     if (v & PCCL_ABORT_BIT) return (int)(v & 0xff);
     if (v >= target) return 0;
     if ((++it & 255u) == 0) {
-      if (*c.P->err != 0) return *c.P->err;
+      if (const uint64_t e = *err_mirror(*c.P, c.r)) return (int)e;
       if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;  // PCCL_ERR_TIMEOUT
     }
   }
@@ -337,7 +352,7 @@ __device__ __forceinline__ int spin_ready(const Ctx &c, const uint64_t *w, int u
     const int r = ready_check(c, ld_acquire_sys(w), unit);
     if (r >= 0) return r;
     if ((++it & 255u) == 0) {
-      if (*c.P->err != 0) return *c.P->err;
+      if (const uint64_t e = *err_mirror(*c.P, c.r)) return (int)e;
       if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;  // PCCL_ERR_TIMEOUT
     }
   }
@@ -483,7 +498,7 @@ __device__ __forceinline__ int ll_wait(const Ctx &c, const uint4 *p, uint32_t ta
     v = ll_ld(p);
     if (ll_ok(v, tag)) return 0;
     if ((++it & 1023u) == 0) {
-      if (*c.P->err != 0) return *c.P->err;
+      if (const uint64_t e = *err_mirror(*c.P, c.r)) return (int)e;
       const uint4 h = ll_ld(hdr);
       if (ll_ok(h, tag) && (h.x != c.P->meta[c.y] || h.z != c.P->meta[c.y])) return 4;
       if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;

@@ -1239,6 +1239,7 @@ struct CeWait {
   const uint64_t *word;
   uint64_t target;
   volatile int *err;
+  volatile uint64_t *mirror;  // this rank's device-side error mirror (WCTRL [PCCL_WCTRL_ERR])
   int64_t timeout_ns;
   int gs;
   uint64_t *meta[PCCL_MAXR];  // per member: META rows of the slot in its arena
@@ -1255,11 +1256,12 @@ __global__ void k_ce_wait(const __grid_constant__ CeWait W) {
       if (v & PCCL_ABORT_BIT) { code = (int)(v & 0xff); break; }
       if (v >= W.target) break;
       if ((++it & 255u) == 0) {
-        if (*W.err != 0) { code = *W.err; break; }
+        if (const uint64_t e = *W.mirror) { code = (int)e; break; }
         if (global_timer_ns() - t0 > (uint64_t)W.timeout_ns) { code = 5; break; }  // PCCL_ERR_TIMEOUT
       }
     }
-    if (code && *W.err == 0) {
+    if (code && *W.mirror == 0) {
+      *W.mirror = (uint64_t)code;
       *W.err = code;
       __threadfence_system();
     }

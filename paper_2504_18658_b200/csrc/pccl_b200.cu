@@ -733,6 +733,7 @@ int ce_all_gather(pccl_comm *c, int algo, const void *send, void *recv, size_t b
   memset(&W, 0, sizeof(W));
   W.target = e;
   W.err = w->err_dev;
+  W.mirror = (uint64_t *)w->segs[0].ptr[me] + PCCL_WCTRL_OFF + PCCL_WCTRL_ERR;
   W.timeout_ns = w->p_timeout_ms * 1000000ll;
   W.gs = gs;
   for (int m = 0; m < gs; ++m)
