@@ -281,8 +281,8 @@ __device__ __forceinline__ void trace_ev(Ctx &c, int kind, int unit) {
 // Flood ABORT into every member's slot (all sources, all CTAs) so that every
 // waiter of this group, on every GPU, wakes up. Called by a whole CTA.
 __device__ __noinline__ void abort_group(const Ctx &c, int code) {
-  if (threadIdx.x == 0 && *err_mirror(*c.P, c.r) == 0) {
-    *c.P->err = code;  // host-visible (the host reports it); written once per rank
+  if (threadIdx.x == 0 && *c.P->err == 0) {  // error path only: reading host memory is fine here
+    *c.P->err = code;  // host-visible (the host reports it)
     __threadfence_system();
   }
   if (threadIdx.x < c.gs)  // every member's device mirror: its spinning CTAs stop without host-memory reads
