@@ -221,6 +221,33 @@ def main() -> int:
                   oracle.hier_reduce_scatter(rs_in, N, M, inter)[rank])
 
     sync_point("hier")
+    # hierarchical launch variants: intra phase ring / direct x chained /
+    # separate phase launches, aligned (chain eligible) and odd sizes, fp32
+    # and bf16 (the direct intra RS folds with the ring's rounding points)
+    for intra, chain in ((1, 1), (1, 0), (0, 0), (0, 1)):
+        comm.world.set_param("hier_intra", intra)
+        comm.world.set_param("hier_chain", chain)
+        for N, M in [(N, M) for N, M in grids if N > 1 and M > 1]:
+            for inter in ("ring", "recursive"):
+                if inter == "recursive" and N & (N - 1):
+                    continue
+                plan = pkg.HierPlan(topo=pkg.Topology(N, M), inter_alg=inter)
+                tag = f"{N}x{M}_{inter}_intra{intra}_chain{chain}"
+                for n in (37, 1000, 65536):
+                    ag_in = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+                    check(f"hierv_ag_{tag}_{n}", pkg.hier_all_gather(plan, comm, ag_in[rank]),
+                          oracle.hier_all_gather(ag_in, N, M, inter)[rank])
+                    rs_in = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+                    check(f"hierv_rs_{tag}_{n}", pkg.hier_reduce_scatter(plan, comm, rs_in[rank]),
+                          oracle.hier_reduce_scatter(rs_in, N, M, inter)[rank])
+                    bf = [oracle.f32_to_bf16(x) for x in rs_in]
+                    got = pkg.hier_reduce_scatter(plan, comm, torch.from_numpy(bf[rank].view(np.int16)).view(
+                        torch.bfloat16).cuda())
+                    check(f"hierv_rs_bf16_{tag}_{n}", got.view(torch.int16).cpu().numpy().view(np.uint16),
+                          oracle.hier_reduce_scatter(bf, N, M, inter, "bf16")[rank])
+    comm.world.set_param("hier_intra", -1)
+    comm.world.set_param("hier_chain", 1)
+    sync_point("hier_variants")
     # back-to-back reuse + barrier
     for it in range(30):
         x = torch.full((4096 * p,), float(it + rank), device="cuda")
