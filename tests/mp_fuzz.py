@@ -98,6 +98,11 @@ def main() -> int:
         kind = rng.choice(["sym", "plain", "misaligned", "host"] if coll != "hier" else ["sym", "plain", "misaligned"])
         w.set_param("item_kib", rng.choice([0, 0, 16, 64]))  # direct kernels: static slices / work items
         w.set_param("rs_variant", rng.choice([-1, -1, 5, 7]))  # 5: pipelined push (direct), 7: work items (recursive)
+        # hierarchical: intra phase auto / ring / direct, chained or separate
+        # phase launches, CTA count default or forced (chaining needs <= 128)
+        w.set_param("hier_intra", rng.choice([-1, 0, 1]))
+        w.set_param("hier_chain", rng.choice([1, 1, 0]))
+        w.set_param("ctas", rng.choice([0, 0, 0, 24, 96, 160]))
         # 5: copy engine (ring / recursive into a registered output; every rank
         # takes the same choice, a call that does not qualify is an error)
         use_ce = ce and coll == "ag" and kind == "sym" and algo != "direct" and rng.random() < 0.4
