@@ -671,6 +671,30 @@ __device__ __forceinline__ void copy_units(char *dst, const char *src, int64_t l
   }
 }
 
+// copy_units that also writes a second destination from the same loads (a
+// push all-gather storing my block into a peer and into my own output: one
+// read of the send buffer, no separate local-copy pass in the tail).
+template <int U, int UNROLL>
+__device__ __forceinline__ void copy_units_dup(char *dst, char *dst2, const char *src, int64_t lo, int64_t hi) {
+  using T = typename VecT<U>::T;
+  T *d = reinterpret_cast<T *>(dst);
+  T *d2 = reinterpret_cast<T *>(dst2);
+  const T *s = reinterpret_cast<const T *>(src);
+  const int nt = blockDim.x;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)UNROLL * nt) {
+    T v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) v[u] = ld_peer(s + i + (int64_t)u * nt);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) d[i + (int64_t)u * nt] = v[u];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (i + (int64_t)u * nt < hi) d2[i + (int64_t)u * nt] = v[u];
+  }
+}
+
 // --------------------------------------------------------------------------
 // reduction units: VEC -> one uint4 (4 fp32 or 8 bf16/f16), else one element.
 // Accumulation is always fp32 with explicit round-to-nearest adds (no

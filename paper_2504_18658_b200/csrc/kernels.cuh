@@ -155,10 +155,13 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec(const __grid_constant__ Lau
 // Push variants write into the peers' (symmetric) recv: the entry handshake
 // means "my recv may be overwritten", the second one "my block has landed".
 // ============================================================================
+// dst2 != nullptr: the same loads are also stored to dst2 (my own output),
+// so a push all-gather needs no separate local-copy pass.
 template <int U>
-__device__ __forceinline__ void store_units(char *dst, const char *src, int64_t lo, int64_t hi) {
+__device__ __forceinline__ void store_units(char *dst, const char *src, int64_t lo, int64_t hi, char *dst2 = nullptr) {
   using T = typename VecT<U>::T;
   T *d = reinterpret_cast<T *>(dst);
+  T *d2 = reinterpret_cast<T *>(dst2);
   const T *s = reinterpret_cast<const T *>(src);
   const int nt = blockDim.x;
   int64_t i = lo + threadIdx.x;
@@ -168,8 +171,16 @@ __device__ __forceinline__ void store_units(char *dst, const char *src, int64_t 
     for (int u = 0; u < kUnroll; ++u) v[u] = __ldg(s + i + (int64_t)u * nt);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) d[i + (int64_t)u * nt] = v[u];
+    if (d2) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) d2[i + (int64_t)u * nt] = v[u];
+    }
   }
-  for (; i < hi; i += nt) d[i] = __ldg(s + i);
+  for (; i < hi; i += nt) {
+    const T v = __ldg(s + i);
+    d[i] = v;
+    if (d2) d2[i] = v;
+  }
 }
 
 template <int U>
@@ -186,15 +197,18 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
     // time; a per-CTA rotation that spreads every GPU over all peers at once
     // measured 1-3 % slower). Each peer is waited for just before the first
     // store into it, not all of them up front.
+    // The local copy of my block rides on the first peer's loads (one read of
+    // send, two stores) instead of a separate pass in the kernel's tail.
     for (int i = 1; i < c.gs; ++i) {
       const int q = (c.gi + i) % c.gs;
       if (!cta_wait(c, q, 0)) return;
       char *dst = P.recv[c.world(q)];
       for (int t = 0; t < P.nsubblk; ++t)
-        store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi);
+        store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi,
+                       (i == 1 && P.local_copy) ? ag_block<U>(P, P.recv[c.r], c.y, c.gi, t) : nullptr);
     }
     cta_signal_mask(c, peers, 1);  // my block (this CTA's slice of it) has landed in your recv
-    if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
+    if (P.local_copy && c.gs < 2) ag_local_copy<U>(c, lo, hi);
     if (!cta_wait_mask(c, peers, 1)) return;
     return;
   }
@@ -442,17 +456,20 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
       int64_t lo, hi;
       cta_subslice(c, t, lo, hi);
       for (int j = 0; j < P.nsubblk; ++j) {
-        // my own block comes from send, or is already in place in recv (local_copy == 0)
-        const char *src = (s == 0 && P.local_copy) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U
-                                                   : ag_block<U>(P, my, c.y, blk, j);
-        copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), src, lo, hi);
+        // my own block comes from send (and is stored into my recv by the
+        // same loads), or is already in place in recv (local_copy == 0)
+        if (s == 0 && P.local_copy)
+          copy_units_dup<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), ag_block<U>(P, my, c.y, blk, j),
+                                     P.send[c.r] + (int64_t)j * P.send_sub_stride * U, lo, hi);
+        else
+          copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), ag_block<U>(P, my, c.y, blk, j), lo, hi);
       }
       cta_signal(c, next, push_unit(s, nsub, t));
     }
   }
   for (int t = 0; t < nsub; ++t)
     if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t))) return;
-  if (P.local_copy) {
+  if (P.local_copy && gs < 2) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
     ag_local_copy<U>(c, lo, hi);
@@ -480,16 +497,22 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
       cta_subslice(c, t, lo, hi);
       for (int i = start; i < start + width; ++i)
         for (int j = 0; j < P.nsubblk; ++j) {
-          const char *src = (i == c.gi && P.local_copy) ? P.send[c.r] + (int64_t)j * P.send_sub_stride * U
-                                                        : ag_block<U>(P, my, c.y, i, j);
-          copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), src, lo, hi);
+          // my own block comes from send; at step 0 the same loads also
+          // store it into my recv (no local-copy pass in the tail)
+          const char *mine = P.send[c.r] + (int64_t)j * P.send_sub_stride * U;
+          if (i == c.gi && P.local_copy && k == 0)
+            copy_units_dup<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), ag_block<U>(P, my, c.y, i, j), mine, lo, hi);
+          else if (i == c.gi && P.local_copy)
+            copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), mine, lo, hi);
+          else
+            copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), ag_block<U>(P, my, c.y, i, j), lo, hi);
         }
       cta_signal(c, partner, push_unit(k, nsub, t));
     }
   }
   for (int t = 0; t < nsub; ++t)
     if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t))) return;
-  if (P.local_copy) {
+  if (P.local_copy && L == 0) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
     ag_local_copy<U>(c, lo, hi);
