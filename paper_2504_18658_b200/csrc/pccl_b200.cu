@@ -1020,16 +1020,19 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     return PCCL_SUCCESS;
   }
   {
-    // auto: pull (peer loads fused with the add, no staging hop) for direct /
-    // recursive halving when the input is symmetric; push for ring, and for
-    // every algorithm when the input is unregistered (no input staging copy).
+    // auto: pull (peer loads fused with the add, no staging hop) for every
+    // algorithm when the input is symmetric; push when it is unregistered (no
+    // input staging copy). The ring's push variant ends with a purely local
+    // step (carry + own chunk -> output) that leaves NVLink idle in the tail:
+    // pull ring measured 580 vs 502 GB/s at p=2 and 597 vs 583 at p=4
+    // (128 MiB bf16, profiles/r2_rs_ring_pull_vs_push.txt).
     int v = (int)w->p_rs_variant;
     if (v == 4) v = -1;  // LL requested but this message does not qualify
     if (v < 0) {
       int seg;
       size_t off;
       const bool send_reg = resolve(w, ranks[0], sends[0], gs * chunk_bytes, &seg, &off);
-      v = (!send_reg || algo == A_RING) ? 1 : 0;
+      v = !send_reg ? 1 : 0;
     }
     pl.variant = v == 1 ? 1 : (v == 5 && algo == A_DIRECT) ? 5 : (v == 7 && algo == A_REC) ? 7 : 0;
   }

@@ -246,13 +246,13 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
         w.set_param("trace", 0)
         w.set_param("ll_max", ll_max)
     assert len(tr) == p
-    # default data movement for symmetric buffers: AG push; RS ring push,
-    # recursive / direct pull. Waits per CTA = the algorithm's steps plus the
-    # push handshakes ("your buffer is free" before the first store, and the
-    # final arrival of the last forwarded block for AG; direct AG waits for
-    # each peer's "free" separately, just before its stores into that peer).
+    # default data movement for symmetric buffers: AG push, RS pull. Waits
+    # per CTA = the algorithm's steps plus the push handshakes ("your buffer
+    # is free" before the first store, and the final arrival of the last
+    # forwarded block for AG; direct AG waits for each peer's "free"
+    # separately, just before its stores into that peer).
     L = steps
-    expect = {("rs", "ring"): L + 1, ("rs", "recursive"): L, ("rs", "direct"): L,
+    expect = {("rs", "ring"): L, ("rs", "recursive"): L, ("rs", "direct"): L,
               ("ag", "ring"): L + 1, ("ag", "recursive"): 2 * L, ("ag", "direct"): p}[(coll, algo)]
     for row in tr:
         for ev in row:
