@@ -53,7 +53,13 @@ import torch  # noqa: E402
 METRIC = "all-gather & reduce-scatter bus GB/s (64–256 MB) at 2/4/8 B200 vs 900 GB/s"
 NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (fallback; nominal 900)
 NVLINK_NOMINAL_GBS = 900.0
-PATTERN_CEILING_GBS = {"recursive": 642.0, "ring": 680.0, "direct": 634.0}  # profiles/r1_engine_probe_p4.md (rs ring pushes)
+# raw traffic-pattern ceilings (tools/probe.py, profiles/r1_engine_probe_p4.md): every
+# reduce-scatter pulls (LDG from the peers) when its input is symmetric
+PATTERN_CEILING_GBS = {"recursive": 642.0, "ring": 642.0, "direct": 634.0}
+# the same kernel at 1 GiB (fixed per-call costs < 2 %): its data phase's own
+# asymptote, RS bf16 (profiles/r2_sweep_p{2,4}.csv)
+ASYMPTOTE_1GIB_GBS = {(2, "direct"): 657.4, (2, "ring"): 657.7, (2, "recursive"): 658.4,
+                      (4, "direct"): 658.6, (4, "ring"): 661.1, (4, "recursive"): 659.5}
 EMU_RANKS = 8
 SEED = 20250425
 P7 = 12 * 4096 * 4096 + 13 * 4096  # GPT-3-style 7B per-layer params (12h^2 + 13h, h = 4096)
@@ -546,8 +552,12 @@ def run_gpu(args):
                 # tools/probe.py / profiles/r1_engine_probe_p4.md)
                 "pattern_ceiling": {"gbs": PATTERN_CEILING_GBS.get(algo), "frac": round(
                     achieved / PATTERN_CEILING_GBS[algo], 4) if algo in PATTERN_CEILING_GBS else None,
-                    "source": "tools/probe.py raw loops at p=4: recursive = bidirectional LDG pull, ring = "
-                              "bidirectional STG push, direct = all-to-all LDG pull"},
+                    "source": "tools/probe.py raw loops at p=4: recursive / ring = bidirectional LDG pull, "
+                              "direct = all-to-all LDG pull"},
+                "asymptote_1gib": {"gbs": ASYMPTOTE_1GIB_GBS.get((p, algo)), "frac": round(
+                    achieved / ASYMPTOTE_1GIB_GBS[(p, algo)], 4) if (p, algo) in ASYMPTOTE_1GIB_GBS else None,
+                    "source": "the same kernel at 1 GiB per rank (per-call fixed costs < 2 %), "
+                              "profiles/r2_sweep_p{2,4}.csv"},
                 "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
                 "algorithmic_bytes_per_launch": int(S * (p - 1) / p), "traffic": None}
     else:
