@@ -567,8 +567,8 @@ def run_gpu(args):
         traffic = args.traffic
         if traffic is None and algo == "recursive" and args.dtype == "bf16" and args.size_mib == 128:
             # dram__bytes_read.sum + dram__bytes_write.sum of this launch, ncu --set full
-            # (profiles/r2_ncu_k_rs_rec_emulated.md): 1.878912 GB + 0.916739 GB
-            traffic = 2795651328
+            # (profiles/r2_ncu_k_rs_rec_emulated.md): 1.878867 GB + 0.915568 GB
+            traffic = 2794435384
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                 "algorithmic_bytes_per_launch": hbm, "traffic": traffic,
