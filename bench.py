@@ -447,6 +447,37 @@ def time_calls(call, steps: int, stream) -> float:
     return e0.elapsed_time(e1) / 1e3 / steps
 
 
+def time_graph(rig, make_call, steps: int) -> float:
+    """Seconds per call with the same `steps` calls captured in ONE CUDA graph
+    and replayed (the collectives are capture-safe: device-side epochs). On
+    this driver an eagerly launched kernel that touched peer memory pays
+    ~3.6 us at its boundary that a kernel inside a graph does not
+    (tools/pdl_probe.cu, profiles/r2_launch_boundary.md)."""
+    side = torch.cuda.Stream(rig.dev)
+    saved = rig.stream
+    rig.stream = side
+    try:
+        call = make_call()
+    finally:
+        rig.stream = saved
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(steps):
+            call()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    rig.barrier()
+    with torch.cuda.stream(side):
+        call()  # device-side rendezvous of the ranks, as in time_calls
+        e0.record(side)
+        g.replay()
+        e1.record(side)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / steps
+
+
 def run_gpu(args):
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -531,6 +562,18 @@ def run_gpu(args):
         rig.verify_rs(sin, sout, seed0, n, dtype, algo, order)
     checks = {"headline": verified}
 
+    # the same calls captured in one CUDA graph (real mode: the launch-boundary
+    # cost it removes only exists for kernels that touch peer memory)
+    graph = None
+    if real and not args.profile:
+        t_graph = rig.max_over_ranks(time_graph(rig, lambda: rig.rs(algo, order, sin, sout, n, code), args.steps))
+        g_ok = rig.verify_rs(sin, sout, seed0, n, dtype, algo, order)
+        checks["headline_graph"] = g_ok
+        graph = {"value": round(busbw(S, p, t_graph), 2), "unit": "GB/s", "ms_per_step": round(t_graph * 1e3, 5),
+                 "verified": g_ok, "gpu_launches": args.steps,
+                 "how": "the same K calls captured in one CUDA graph and replayed (eager launches of kernels that "
+                        "touch peer memory pay ~3.6 us each at the launch boundary, tools/pdl_probe.cu)"}
+
     extra = {} if args.no_extra else run_extras(args, rig, p, S, n, dtype, code, checks)
 
     # ---- e2e through the public API with host buffers ----
@@ -613,6 +656,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
+            "graph_replay": graph,
             "clocks": clocks.summary(),
             "autotune": autotuned,
             "extra": extra,

@@ -113,7 +113,7 @@ struct LaunchParams {
 
 #define PCCL_TRACE_EVENTS 128
 #define PCCL_TRACE_LAUNCHES 8
-enum TraceKind { TR_START = 1, TR_WAIT = 2, TR_SIGNAL = 3, TR_END = 4, TR_EXIT = 5, TR_RESIDENT = 6 };
+enum TraceKind { TR_START = 1, TR_WAIT = 2, TR_SIGNAL = 3, TR_END = 4, TR_EXIT = 5, TR_RESIDENT = 6, TR_EPILOGUE = 7, TR_PDL = 8 };
 
 // --------------------------------------------------------------------------
 // memory-model primitives
@@ -190,6 +190,7 @@ __device__ __forceinline__ void st_release_gpu(uint64_t *p, uint64_t v) {
 __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   const uint64_t t_resident = P.trace ? global_timer_ns() : 0;  // CTA scheduled (before the PDL wait)
   if (P.chain != 2) pdl_wait();
+  const uint64_t t_pdl = P.trace ? global_timer_ns() : 0;  // the previous grid is complete
   pdl_launch_dependents();
   Ctx c;
   c.P = &P;
@@ -235,6 +236,7 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   }
   if (c.tr && threadIdx.x == 0) {
     c.tr[c.ntr++] = (t_resident << 16) | (TR_RESIDENT << 12);
+    c.tr[c.ntr++] = (t_pdl << 16) | (TR_PDL << 12);
     c.tr[c.ntr++] = (c.t0 << 16) | (TR_START << 12);
   }
   return c;
@@ -268,6 +270,7 @@ struct CtaEpilogue {
             if ((c.ll_peers >> q) & 1u) lc[q] = lc[q] + 1;
         }
       }
+      if (c.tr && c.ntr < PCCL_TRACE_EVENTS) c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)TR_EPILOGUE << 12);
     }
   }
 };

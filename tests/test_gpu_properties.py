@@ -256,7 +256,7 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
               ("ag", "ring"): L + 1, ("ag", "recursive"): 2 * L, ("ag", "direct"): p}[(coll, algo)]
     for row in tr:
         for ev in row:
-            kinds = [k for _, k, _ in ev if k not in (5, 6)]  # (5 CTA exit, 6 resident: timing only)
+            kinds = [k for _, k, _ in ev if k not in (5, 6, 7, 8)]  # (exit, resident, epilogue, PDL release: timing only)
             assert kinds[0] == 1 and kinds.count(2) == expect, (coll, algo, p, kinds)
 
 

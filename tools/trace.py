@@ -40,7 +40,7 @@ def main():
     w.set_param("trace", 1)
     for _ in range(3): f()   # trace keeps the last launch
     torch.cuda.synchronize()
-    tr = [[[e for e in ev if e[1] not in (5, 6)] for ev in w.trace()[0]]][0]
+    tr = [[[e for e in ev if e[1] not in (5, 6, 7, 8)] for ev in w.trace()[0]]][0]
     # per CTA: relative times of the k-th event
     import statistics
     nev = min(len(ev) for ev in tr)

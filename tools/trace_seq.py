@@ -101,12 +101,14 @@ def main():
     launches = [w.trace(back)[0] for back in range(K - 1, -1, -1)]  # oldest first
     w.set_param("trace", 0)
     lines = [f"rank {rank}: event-timed {per_call:.1f} us per call"]
-    prev_exit = None
+    prev_exit = prev_epi = None
     t_base = min(ev[0][0] for ev in launches[0] if ev)
     for i, ctas in enumerate(launches):
         res = [next(t for t, kd, _ in ev if kd == 6) for ev in ctas]
         st0 = [next(t for t, kd, _ in ev if kd == 1) for ev in ctas]
         ex = [next(t for t, kd, _ in ev if kd == 5) for ev in ctas]
+        pdl = [next((t for t, kd, _ in ev if kd == 8), None) for ev in ctas]
+        epi = [t for ev in ctas for t, kd, _ in ev if kd == 7]
         waits = {}
         for ev in ctas:
             s0 = next(t for t, kd, _ in ev if kd == 1)
@@ -116,11 +118,17 @@ def main():
         phase = " ".join(f"{'WSE'[kd - 2]}{u}={statistics.mean(v):.1f}/{max(v):.1f}" for (kd, u), v in
                          sorted(waits.items(), key=lambda kv: statistics.mean(kv[1])))
         gap = (min(st0) - prev_exit) / 1e3 if prev_exit is not None else float("nan")
+        # gap split: last exit -> last epilogue (exit counter atomic) -> PDL release -> start (epoch read)
+        split = ""
+        if prev_exit is not None and prev_epi and all(pdl):
+            split = (f" [exit->epi {(prev_epi - prev_exit) / 1e3:.1f}, epi->pdl {(min(pdl) - prev_epi) / 1e3:.1f},"
+                     f" pdl->start {(min(st0) - min(pdl)) / 1e3:.1f}]")
         lines.append(f"  L{i}: resident {(min(res) - t_base) / 1e3:8.1f} start {(min(st0) - t_base) / 1e3:8.1f}"
                      f"..{(max(st0) - t_base) / 1e3:8.1f} exit mean {(statistics.mean(ex) - t_base) / 1e3:8.1f} "
                      f"max {(max(ex) - t_base) / 1e3:8.1f} span {(max(ex) - min(st0)) / 1e3:6.1f} "
-                     f"gap {gap:5.1f} | {phase}")
+                     f"gap {gap:5.1f}{split} | {phase}")
         prev_exit = max(ex)
+        prev_epi = max(epi) if epi else None
     outs = [None] * p
     dist.all_gather_object(outs, "\n".join(lines))
     if rank == 0:
