@@ -34,7 +34,8 @@
 #define PCCL_CTRL_OFF (4 * PCCL_MAXR * PCCL_MAX_CTAS)
 #define PCCL_SLOT_WORDS (PCCL_CTRL_OFF + 64)  // + CTRL: [0] last completed epoch, [1] CTA exit counter,
                                               //   [2] work-item counter (direct kernels, see for_items),
-                                              //   [3..10] per-step item counters (k_rs_rec_items)
+                                              //   [3..10] per-step item counters (k_rs_rec_items),
+                                              //   [11] CTAs done with the final unit (cta_signal_rank)
 #define PCCL_SLOT_BYTES (PCCL_SLOT_WORDS * 8)
 // After the slots: world-level control words, then the LL (low-latency)
 // message regions (see "LL protocol" below). Both live in segment 0, so every
@@ -410,6 +411,31 @@ __device__ __forceinline__ void cta_signal_mask(Ctx &c, uint32_t mask, int unit)
   const int m = threadIdx.x;
   if (m < c.gs && ((mask >> m) & 1u))
     st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, c.b), ready_value(c, unit));
+  trace_ev(c, TR_SIGNAL, unit);
+}
+// Rank-level publish of a push kernel's FINAL unit: every CTA releases its
+// stores at gpu scope into a counter in my slot (CTRL[11]) and the row's last
+// CTA publishes once per member with a system-scope release into the word of
+// CTA 0 (the acq_rel RMW chain + the CTA barrier make that release
+// cumulative over every CTA's stores). One MEMBAR.SYS per rank instead of
+// one per CTA and member: 128 CTAs issuing system fences at once cost
+// ~4-5 us (profiles/r2_launch_boundary.md). Waiters use cta_wait_mask(...,
+// idx = 0). For a final unit only: a receiver now waits for all of a
+// sender's CTAs, which a pipelined step cannot afford.
+__device__ __forceinline__ void cta_signal_rank(Ctx &c, uint32_t mask, int unit) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(c.my_slot + PCCL_CTRL_OFF) + 11;
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+    s_last = old == (unsigned long long)(c.P->ctas - 1);
+    if (s_last) *reinterpret_cast<volatile unsigned long long *>(ctr) = 0;  // next launch: after this grid
+  }
+  __syncthreads();
+  const int m = threadIdx.x;
+  if (s_last && m < c.gs && ((mask >> m) & 1u))
+    st_release_sys(Ctx::word(c.slot_in(m), F_READY, c.gi, 0), ready_value(c, unit));
   trace_ev(c, TR_SIGNAL, unit);
 }
 // Pull kernels publish data that lives in the writer's OWN memory: once a

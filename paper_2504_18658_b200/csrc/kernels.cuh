@@ -207,9 +207,9 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
         store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi,
                        (i == 1 && P.local_copy) ? ag_block<U>(P, P.recv[c.r], c.y, c.gi, t) : nullptr);
     }
-    cta_signal_mask(c, peers, 1);  // my block (this CTA's slice of it) has landed in your recv
+    cta_signal_rank(c, peers, 1);  // my whole block has landed in your recv (one system release per rank)
     if (P.local_copy && c.gs < 2) ag_local_copy<U>(c, lo, hi);
-    if (!cta_wait_mask(c, peers, 1)) return;
+    if (!cta_wait_mask(c, peers, 1, 0)) return;
     return;
   }
   if (!cta_wait_mask(c, peers, 0)) return;
@@ -226,9 +226,9 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
                      a, e);
     });
   }
-  cta_signal_mask(c, peers, 1);  // my block (this CTA's items of it) has landed in your recv
+  cta_signal_rank(c, peers, 1);  // my whole block has landed in your recv (one system release per rank)
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
-  if (!cta_wait_mask(c, peers, 1)) return;
+  if (!cta_wait_mask(c, peers, 1, 0)) return;
 }
 
 struct TmaCfg {
