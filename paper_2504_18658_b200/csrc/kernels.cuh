@@ -464,11 +464,18 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
         else
           copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), ag_block<U>(P, my, c.y, blk, j), lo, hi);
       }
-      cta_signal(c, next, push_unit(s, nsub, t));
+      if (s == gs - 2 && nsub == 1)
+        cta_signal_rank(c, 1u << next, push_unit(s, nsub, t));  // final unit: one system release per rank
+      else
+        cta_signal(c, next, push_unit(s, nsub, t));
     }
   }
-  for (int t = 0; t < nsub; ++t)
-    if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t))) return;
+  if (gs > 1 && nsub == 1) {
+    if (!cta_wait_mask(c, 1u << prev, push_unit(gs - 2, 1, 0), 0)) return;
+  } else {
+    for (int t = 0; t < nsub; ++t)
+      if (!cta_wait(c, prev, push_unit(gs - 2, nsub, t))) return;
+  }
   if (P.local_copy && gs < 2) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
@@ -507,11 +514,18 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
           else
             copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), ag_block<U>(P, my, c.y, i, j), lo, hi);
         }
-      cta_signal(c, partner, push_unit(k, nsub, t));
+      if (k == L - 1 && nsub == 1)
+        cta_signal_rank(c, 1u << partner, push_unit(k, nsub, t));  // final unit: one system release per rank
+      else
+        cta_signal(c, partner, push_unit(k, nsub, t));
     }
   }
-  for (int t = 0; t < nsub; ++t)
-    if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t))) return;
+  if (L > 0 && nsub == 1) {
+    if (!cta_wait_mask(c, 1u << recdbl_partner(c.gi, L - 1), push_unit(L - 1, 1, 0), 0)) return;
+  } else {
+    for (int t = 0; t < nsub; ++t)
+      if (!cta_wait(c, recdbl_partner(c.gi, L - 1), push_unit(L - 1, nsub, t))) return;
+  }
   if (P.local_copy && L == 0) {
     int64_t lo, hi;
     split32(P.blk, P.ctas, c.b, lo, hi);
