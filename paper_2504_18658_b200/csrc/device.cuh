@@ -86,6 +86,8 @@ struct LaunchParams {
   uint32_t tma_tile;  // TMA tile bytes
   int local_fence;  // 1: pull-kernel signals fence at gpu scope (data is in the writer's own HBM)
   int wire;         // direct RS fold: round the partial to the storage type after every add (= step-wise algorithms)
+  int rank_final;   // push AG: publish the final unit rank-level (cta_signal_rank); flat calls only (a
+                    //   per-call SPMD-uniform choice: hierarchical phases may chain on some ranks only)
   int chain;        // 1: first launch of a chained pair (publishes per-CTA completion), 2: second (waits for it
                     //    instead of the PDL grid-completion wait); see "chained launches" below
   int64_t item;     // direct kernels: units per dynamically claimed work item (0: static CTA slices)

@@ -207,9 +207,16 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
         store_units<U>(ag_block<U>(P, dst, c.y, c.gi, t), P.send[c.r] + (int64_t)t * P.send_sub_stride * U, lo, hi,
                        (i == 1 && P.local_copy) ? ag_block<U>(P, P.recv[c.r], c.y, c.gi, t) : nullptr);
     }
-    cta_signal_rank(c, peers, 1);  // my whole block has landed in your recv (one system release per rank)
+    // Final publish: rank-level (one system release per rank) for flat calls;
+    // per CTA in hierarchical phases, where a chained second launch's CTA b
+    // starts as soon as this CTA b is done.
+    if (P.rank_final) {
+      cta_signal_rank(c, peers, 1);
+    } else {
+      cta_signal_mask(c, peers, 1);
+    }
     if (P.local_copy && c.gs < 2) ag_local_copy<U>(c, lo, hi);
-    if (!cta_wait_mask(c, peers, 1, 0)) return;
+    if (!cta_wait_mask(c, peers, 1, P.rank_final ? 0 : -1)) return;
     return;
   }
   if (!cta_wait_mask(c, peers, 0)) return;
@@ -226,9 +233,13 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_push(const __grid_consta
                      a, e);
     });
   }
-  cta_signal_rank(c, peers, 1);  // my whole block has landed in your recv (one system release per rank)
+  if (P.rank_final) {
+    cta_signal_rank(c, peers, 1);  // my whole block has landed in your recv (one system release per rank)
+  } else {
+    cta_signal_mask(c, peers, 1);
+  }
   if (P.local_copy) ag_local_copy<U>(c, lo, hi);  // overlaps the peers' stores in flight
-  if (!cta_wait_mask(c, peers, 1, 0)) return;
+  if (!cta_wait_mask(c, peers, 1, P.rank_final ? 0 : -1)) return;
 }
 
 struct TmaCfg {
@@ -464,13 +475,13 @@ __global__ void __launch_bounds__(kThreads) k_ag_ring_push(const __grid_constant
         else
           copy_units<U, kUnroll>(ag_block<U>(P, nx, c.y, blk, j), ag_block<U>(P, my, c.y, blk, j), lo, hi);
       }
-      if (s == gs - 2 && nsub == 1)
+      if (s == gs - 2 && nsub == 1 && P.rank_final)
         cta_signal_rank(c, 1u << next, push_unit(s, nsub, t));  // final unit: one system release per rank
       else
         cta_signal(c, next, push_unit(s, nsub, t));
     }
   }
-  if (gs > 1 && nsub == 1) {
+  if (gs > 1 && nsub == 1 && P.rank_final) {
     if (!cta_wait_mask(c, 1u << prev, push_unit(gs - 2, 1, 0), 0)) return;
   } else {
     for (int t = 0; t < nsub; ++t)
@@ -514,13 +525,13 @@ __global__ void __launch_bounds__(kThreads) k_ag_rec_push(const __grid_constant_
           else
             copy_units<U, kUnroll>(ag_block<U>(P, pr, c.y, i, j), ag_block<U>(P, my, c.y, i, j), lo, hi);
         }
-      if (k == L - 1 && nsub == 1)
+      if (k == L - 1 && nsub == 1 && P.rank_final)
         cta_signal_rank(c, 1u << partner, push_unit(k, nsub, t));  // final unit: one system release per rank
       else
         cta_signal(c, partner, push_unit(k, nsub, t));
     }
   }
-  if (L > 0 && nsub == 1) {
+  if (L > 0 && nsub == 1 && P.rank_final) {
     if (!cta_wait_mask(c, 1u << recdbl_partner(c.gi, L - 1), push_unit(L - 1, 1, 0), 0)) return;
   } else {
     for (int t = 0; t < nsub; ++t)

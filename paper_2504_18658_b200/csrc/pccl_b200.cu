@@ -320,6 +320,7 @@ struct Plan {
   uint32_t place = 0;  // symmetric-placement hash (real mode)
   int variant = 0;
   int wire = 0;        // direct RS: round after every add (step-wise rounding points)
+  int rank_final = 0;  // push AG final unit published rank-level (flat calls)
   int chain = 0;       // chained pair (device.cuh): 1 first launch, 2 second launch
   uint32_t chain_slot_off[PCCL_MAXR] = {};  // chain 1, per row: the second group's slot (words)
   int force_ctas = 0;  // > 0: CTAs per row (chained launches must cut identical slices)
@@ -340,6 +341,7 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.local_fence = (int)w->p_local_fence;
   P.wire = pl.wire;
   P.chain = pl.chain;
+  P.rank_final = pl.rank_final;
   P.tma_stages = (int)w->p_tma_stages;
   P.tma_tile = (uint32_t)w->p_tma_tile;
 
@@ -924,6 +926,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
     }
     if (algo != A_DIRECT && v != 1) v = 0;  // TMA variants exist for direct only
     pl.variant = v;
+    pl.rank_final = 1;  // flat call: every rank takes the same choice
   }
   Binder B{w, stream};
   std::vector<std::pair<char *, char *>> copy_out;  // (staged recv, user recv)
