@@ -70,6 +70,7 @@ __global__ void k_body(unsigned long long *local, unsigned long long *peer, int 
   }
 }
 
+static int g_domain = 0;  // 1: launch in the "remote" memory-synchronization domain
 static float run_eager(int mode, int ctas, int threads, bool pdl, unsigned long long *local,
                        unsigned long long *peer, char *buf, cudaStream_t s) {
   const int K = 1000;
@@ -77,11 +78,14 @@ static float run_eager(int mode, int ctas, int threads, bool pdl, unsigned long 
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(threads);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeMemSyncDomain;
+  attr[1].val.memSyncDomain = g_domain ? cudaLaunchMemSyncDomainRemote : cudaLaunchMemSyncDomainDefault;
+  if (!pdl) attr[0] = attr[1];
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (pdl ? 1 : 0) + 1;
   // a long first kernel lets the host queue all K launches before they run
   for (int i = 0; i < 20; ++i) CK(cudaLaunchKernelEx(&cfg, k_body, local, peer, mode, buf));
   cudaEvent_t a, b;
@@ -240,8 +244,10 @@ int main(int argc, char **argv) {
       const float e = run_eager(mode, 128, 512, true, local, peer, buf, s);
       const float f = vpeer ? run_eager(mode, 128, 512, true, local, vpeer, buf, s) : -1.f;
       const float gv = vpeer ? run(mode, 128, 512, true, local, vpeer, buf, s) : -1.f;
-      const float h = run_graph1(mode, 128, 512, true, local, peer, buf, s);
-      printf("  %-22s  1x32 pdl %6.2f   128x512 pdl %6.2f   no-pdl %6.2f   eager pdl %6.2f   1-node graphs %6.2f"
+      g_domain = 1;
+      const float h = run_eager(mode, 128, 512, true, local, peer, buf, s);
+      g_domain = 0;
+      printf("  %-22s  1x32 pdl %6.2f   128x512 pdl %6.2f   no-pdl %6.2f   eager pdl %6.2f   eager remote-domain %6.2f"
              "   VMM peer: graph %6.2f eager %6.2f\n", names[mode], a, b, c, e, h, gv, f);
     }
     CK(cudaStreamDestroy(s));
