@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--iters", type=int, default=100000, help="collectives per (local_fence) setting")
     ap.add_argument("--fences", default="1,0")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--movement", choices=["pull", "default"], default="pull",
+                    help="pull: force pull kernels (the local_fence publish); default: the library's choice")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
@@ -40,8 +42,11 @@ def main():
     comm = pkg.init_from_torch(device=dev.index)
     w = comm.world
     w.set_param("ll_max", 0)        # flag protocol only (LL carries its flags inside the data)
-    w.set_param("rs_variant", 0)    # pull
-    w.set_param("ag_variant", 0)    # pull
+    if a.movement == "pull":
+        w.set_param("rs_variant", 0)    # pull
+        w.set_param("ag_variant", 0)    # pull
+    # "default": the library's choice for symmetric buffers (RS pull, AG push
+    # with the rank-level final publish)
     stream = torch.cuda.current_stream(dev).cuda_stream
     pow2 = p & (p - 1) == 0
     algos = ["direct", "ring"] + (["recursive"] if pow2 else [])
@@ -104,7 +109,7 @@ def main():
         report.append(f"local_fence={fence}: {a.iters} calls per rank in {dt:.1f} s, mismatched elements "
                       f"(all ranks) = {int(tot)}; mix " + ", ".join(f"{k[0]}/{k[1]} {v}" for k, v in sorted(counts.items())))
     if rank == 0:
-        print(f"== litmus p={p} sizes {[s >> 10 for s in sizes]} KiB, pull kernels, flag protocol", flush=True)
+        print(f"== litmus p={p} sizes {[s >> 10 for s in sizes]} KiB, {a.movement} data movement, flag protocol", flush=True)
         for r in report:
             print("  " + r, flush=True)
     dist.barrier()
