@@ -440,6 +440,15 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   P.send_sub_stride = units(pl.send_sub_stride);
   P.out_sub_stride = units(pl.out_sub_stride);
 
+  // Multi-step protocols hand CTA b's slice of step k to the partner's CTA b
+  // at step k + 1, so every rank must cut the same slices: the unit size
+  // (from this rank's own buffer alignment in real mode) joins the call
+  // signature, and a rank whose buffers are aligned differently raises
+  // LengthMismatch everywhere instead of racing. Direct (one-step) kernels
+  // only wait on whole CTAs and tolerate it.
+  int u_code = 0;
+  if (pl.algo != A_DIRECT)
+    for (int b = U; b > 1; b >>= 1) ++u_code;
   // ---- rows
   const int nrows = (int)pl.rows.size();
   for (int y = 0; y < nrows; ++y) {
@@ -456,7 +465,8 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     P.slot_off[y] = (uint32_t)((size_t)g->slot * PCCL_SLOT_WORDS);
     P.chain_slot_off[y] = pl.chain_slot_off[y];
     P.epoch[y] = 0;  // device-side (CTRL word of the slot), see make_ctx
-    P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order | (pl.wire << 4), pl.count, pl.dtype, pl.gs) ^
+    P.meta[y] = (hash_meta(pl.coll, pl.algo * 16 + pl.variant, pl.order | (pl.wire << 4) | (u_code << 5), pl.count,
+                           pl.dtype, pl.gs) ^
                  (pl.place * 2654435761u) ^
                  w->meta_skew[rw.rank]) & 0x7fffffffu;
   }

@@ -436,6 +436,30 @@ def main() -> int:
     # cross-rank length mismatch must raise LengthMismatch (device-side check)
     from paper_2504_18658_b200.errors import LengthMismatch
 
+    # a multi-step collective whose buffers are aligned differently on one
+    # rank (here rank 0's output sits 4 bytes into its allocation) cuts other
+    # slices there: detected through the call signature on every rank, and
+    # the world recovers after a collective flag reset
+    n = 4096
+    xin = torch.ones(n * p, device="cuda")
+    buf = torch.empty(n + 4, device="cuda")
+    yout = buf[1:1 + n] if rank == 0 else buf[:n]
+    try:
+        pkg.ring_reduce_scatter(comm, xin, out=yout)
+        torch.cuda.synchronize()
+        comm.world.check()
+        failures.append("alignment_mismatch_not_detected")
+    except LengthMismatch:
+        pass
+    torch.cuda.synchronize()
+    dist.barrier()
+    comm.world.reset_flags()
+    dist.barrier()
+    y2 = pkg.ring_reduce_scatter(comm, xin)  # the world works again
+    torch.cuda.synchronize()
+    if not torch.equal(y2, torch.full((n,), float(p), device="cuda")):
+        failures.append("after_alignment_mismatch_reset")
+
     try:
         pkg.direct_all_gather(comm, np.zeros(4 if rank == 0 else 2, np.float32))
         failures.append("mismatch_not_detected")
