@@ -515,6 +515,10 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     if (pl.chain && ctas != pl.force_ctas) return PCCL_ERR_UNSUPPORTED;  // chained slices must match (host checks caps)
   }
   P.ctas = ctas;
+  // every flag is per (source, CTA index): the CTA count is part of the call
+  // signature (a rank launching another count raises LengthMismatch instead
+  // of waiting for CTAs that do not exist until the timeout)
+  for (int y = 0; y < nrows; ++y) P.meta[y] = (P.meta[y] ^ ((uint32_t)ctas * 0x9E3779B1u)) & 0x7fffffffu;
   if (pl.variant == 7) {  // recursive halving with per-step work items: ~items_per_cta items per CTA
     const int64_t target = std::min<int64_t>(PCCL_MAX_CTAS, std::max<int64_t>(1, w->p_items_per_cta * ctas));
     const int64_t it = (P.blk + target - 1) / target;
@@ -1141,8 +1145,12 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
   // Chain the two phases (device.cuh "chained launches") when both exist, the
   // slices of both launches are identical (16-byte units everywhere, static
   // slices, the same CTA count) and PDL is on.
-  bool chain = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
-               w->p_ctas <= 128 && (count * es) % 16 == 0;
+  // The CTA count is fixed by SPMD-uniform conditions only; whether the two
+  // launches are chained also depends on this rank's pointers, which only
+  // changes local sequencing.
+  const bool uniform = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
+                       w->p_ctas <= 128 && (count * es) % 16 == 0;
+  bool chain = uniform;
   for (size_t i = 0; chain && i < ranks.size(); ++i)
     chain = ((uintptr_t)outp[ranks[i]] % 16 == 0) && ((uintptr_t)sends[i] % 16 == 0);
   const int chain_ctas = w->p_ctas > 0 ? (int)w->p_ctas : 128;
@@ -1150,9 +1158,9 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
   // their global positions (g*count) directly (fused shuffle)
   if (N > 1) {
     Plan pl;
+    if (uniform) pl.force_ctas = chain_ctas;
     if (chain) {
       pl.chain = 1;
-      pl.force_ctas = chain_ctas;
       for (size_t i = 0; i < ranks.size(); ++i) {  // row i: the intra group of ranks[i] runs phase 2
         const int nd = topo[ranks[i]] / M;
         std::vector<int> grp;
@@ -1196,10 +1204,8 @@ int do_hier_all_gather(pccl_world *w, const std::vector<int> &mem, int N, int M,
     const bool direct = w->p_hier_intra == 1 || (w->p_hier_intra < 0 && M >= 3);
     pl.coll = PCCL_ALL_GATHER; pl.algo = direct ? A_DIRECT : A_RING; pl.dtype = dtype; pl.count = (size_t)N * count;
     pl.gs = M;
-    if (chain) {
-      pl.chain = 2;
-      pl.force_ctas = chain_ctas;
-    }
+    if (uniform) pl.force_ctas = chain_ctas;
+    if (chain) pl.chain = 2;
     pl.nsubblk = N; pl.blk = (int64_t)count; pl.sub_stride = (int64_t)M * count; pl.istride = (int64_t)count;
     pl.send_sub_stride = (int64_t)count; pl.local_copy = 0; pl.place = place;
     pl.variant = w->p_ag_variant == 0 ? 0 : 1;
@@ -1250,8 +1256,10 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
   }
   const uint32_t place = w->emu ? 0 : B.place;
   // chained phases (see do_hier_all_gather)
-  bool chain = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
-               w->p_ctas <= 128 && (n * es) % 16 == 0 && w->p_rs_variant != 1;
+  // (CTA count from SPMD-uniform conditions only, see do_hier_all_gather)
+  const bool uniform = !w->emu && w->p_pdl && w->p_hier_chain && N > 1 && M > 1 && w->p_item_kib == 0 &&
+                       w->p_ctas <= 128 && (n * es) % 16 == 0 && w->p_rs_variant != 1;
+  bool chain = uniform;
   for (size_t i = 0; chain && i < ranks.size(); ++i)
     chain = ((uintptr_t)sendp[ranks[i]] % 16 == 0) && ((uintptr_t)recvs[i] % 16 == 0);
   const int chain_ctas = w->p_ctas > 0 ? (int)w->p_ctas : 128;
@@ -1267,9 +1275,9 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
     pl.gs = M;
     pl.order = O_RING;
     pl.wire = 1;
+    if (uniform) pl.force_ctas = chain_ctas;
     if (chain) {
       pl.chain = 1;
-      pl.force_ctas = chain_ctas;
       for (size_t i = 0; i < ranks.size(); ++i) {  // row i: the inter group of ranks[i] runs phase 2
         const int j = topo[ranks[i]] % M;
         std::vector<int> grp;
@@ -1310,10 +1318,8 @@ int do_hier_reduce_scatter(pccl_world *w, const std::vector<int> &mem, int N, in
   if (N > 1) {
     Plan pl;
     pl.coll = PCCL_REDUCE_SCATTER; pl.algo = inter; pl.dtype = dtype; pl.count = n; pl.gs = N;
-    if (chain) {
-      pl.chain = 2;
-      pl.force_ctas = chain_ctas;
-    }
+    if (uniform) pl.force_ctas = chain_ctas;
+    if (chain) pl.chain = 2;
     pl.blk = (int64_t)n; pl.istride = (int64_t)n; pl.out_sub_stride = (int64_t)n; pl.place = place;
     for (size_t i = 0; i < ranks.size(); ++i) {
       const int r = ranks[i], j = topo[r] % M;
