@@ -51,9 +51,10 @@ __global__ void k_pingpong(unsigned long long *me, unsigned long long *other, in
       }
       publish(other, v, smode);
     }
-    if (pmode == 1) {
+    if (pmode == 1) {  // the acquire that the relaxed polling defers
       unsigned long long w;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(me) : "memory");
+      if (w == ~0ull) *ns = -1;
     }
   }
   unsigned long long t_end;
