@@ -436,3 +436,37 @@ def test_nvls_needs_real_mode():
     assert not nvls.nvls_supported(w)
     with pytest.raises(Unsupported):
         nvls.create_nvls_segment(w, 1 << 20)
+
+
+@pytest.mark.parametrize("algo", ["direct", "ring", "recursive"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_push_all_gather_mixed_in_place_rows(algo, dtype):
+    """Push all-gathers store the own block into the output from the first
+    push's loads (no tail local copy). In one emulated launch some rows run
+    in place (send = own block of the output) and others do not: the copy is
+    one value per launch (OR over the rows), a self-copy is harmless, and
+    every output is exact."""
+    pkg = _pkg()
+    p, n = 4, 40000 + 8
+    w = pkg.emulated_world(p)
+    full = w.empty(n * p, dtype)
+    sends = w.empty(n, dtype)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    blocks = [torch.randn(n, generator=g, device="cuda").to(dtype) for _ in range(p)]
+    for r in range(p):
+        full[r].fill_(float("nan"))
+        if r % 2 == 0:
+            full[r][r * n:(r + 1) * n].copy_(blocks[r])  # in place
+        else:
+            sends[r].copy_(blocks[r])
+
+    def body(c):
+        src = full[c.rank][c.rank * n:(c.rank + 1) * n] if c.rank % 2 == 0 else sends[c.rank]
+        pkg.all_gather_into_tensor(full[c.rank], src, c, algorithm=algo)
+        return None
+
+    pkg.run_ranks(p, body)
+    want = torch.cat(blocks)
+    for r in range(p):
+        assert torch.equal(full[r].view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                           want.view(torch.int16 if dtype == torch.bfloat16 else torch.int32)), (algo, r)
