@@ -566,13 +566,18 @@ def run_gpu(args):
     # cost it removes only exists for kernels that touch peer memory)
     graph = None
     if real and not args.profile:
-        t_graph = rig.max_over_ranks(time_graph(rig, lambda: rig.rs(algo, order, sin, sout, n, code), args.steps))
-        g_ok = rig.verify_rs(sin, sout, seed0, n, dtype, algo, order)
-        checks["headline_graph"] = g_ok
-        graph = {"value": round(busbw(S, p, t_graph), 2), "unit": "GB/s", "ms_per_step": round(t_graph * 1e3, 5),
-                 "verified": g_ok, "gpu_launches": args.steps,
-                 "how": "the same K calls captured in one CUDA graph and replayed (eager launches of kernels that "
-                        "touch peer memory pay ~3.6 us each at the launch boundary, tools/pdl_probe.cu)"}
+        try:
+            t_graph = rig.max_over_ranks(time_graph(rig, lambda: rig.rs(algo, order, sin, sout, n, code),
+                                                    args.steps))
+            g_ok = rig.verify_rs(sin, sout, seed0, n, dtype, algo, order)
+            checks["headline_graph"] = g_ok
+            graph = {"value": round(busbw(S, p, t_graph), 2), "unit": "GB/s",
+                     "ms_per_step": round(t_graph * 1e3, 5), "verified": g_ok, "gpu_launches": args.steps,
+                     "how": "the same K calls captured in one CUDA graph and replayed (eager launches of kernels "
+                            "that touch peer memory pay ~3.6 us each at the launch boundary, tools/pdl_probe.cu)"}
+        except Exception as exc:  # noqa: BLE001 - a secondary number never costs the headline line
+            graph = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:200]}
+            rig.world.check()  # a device error still surfaces
 
     extra = {} if args.no_extra else run_extras(args, rig, p, S, n, dtype, code, checks)
 
