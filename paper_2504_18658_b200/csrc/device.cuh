@@ -41,7 +41,7 @@
 // message regions (see "LL protocol" below). Both live in segment 0, so every
 // peer already has them mapped.
 #define PCCL_WCTRL_OFF ((size_t)PCCL_NSLOTS * PCCL_SLOT_WORDS)  // words: [q] LL messages exchanged with world rank q
-#define PCCL_WCTRL_WORDS 64
+#define PCCL_WCTRL_WORDS 128
 #define PCCL_LL_OFF (PCCL_WCTRL_OFF + PCCL_WCTRL_WORDS)  // words
 #define PCCL_LL_HDR_BYTES 256
 #define PCCL_LL_MAX_PAYLOAD ((size_t)1 << 20)  // payload bytes per (src -> dst) message
@@ -59,7 +59,16 @@
 // it instead of the host-mapped error word: 128 CTAs reading host memory at
 // once stalled a kernel's exits by up to 120 us (profiles/r2_overhead_p4.md).
 #define PCCL_WCTRL_ERR 48
-#define PCCL_FLAG_BYTES (PCCL_MBOX_OFF + (size_t)PCCL_MAXR * PCCL_MBOX_BYTES)
+// After the mailboxes: the LL128 message regions (line protocol for mid-size
+// direct all-gathers, "LL128" below). Separate from the LL regions so that a
+// receiver of one format never polls stale payload of the other; its channel
+// counters are WCTRL [64 + q].
+#define PCCL_WCTRL_LL128 64
+#define PCCL_LL128_LINES 16384  // 128-byte lines per message (2 MiB)
+#define PCCL_LL128_MAX_PAYLOAD ((size_t)PCCL_LL128_LINES * 120)
+#define PCCL_LL128_REGION_BYTES (PCCL_LL_HDR_BYTES + (size_t)PCCL_LL128_LINES * 128)
+#define PCCL_LL128_OFF (PCCL_MBOX_OFF + (size_t)PCCL_MAXR * PCCL_MBOX_BYTES)  // bytes
+#define PCCL_FLAG_BYTES (PCCL_LL128_OFF + (size_t)2 * PCCL_MAXR * PCCL_LL128_REGION_BYTES)
 #define PCCL_ABORT_BIT (1ull << 63)
 
 namespace pccl {
@@ -155,6 +164,7 @@ struct Ctx {
   uint64_t *tr;  // trace cursor base (nullptr: tracing off)
   int ntr;
   uint32_t ll_peers;  // LL kernels: world ranks whose channel counter the last CTA advances
+  int ll_ctr;         // WCTRL index of those counters: 0 (LL) or PCCL_WCTRL_LL128
   uint64_t chain_epoch;  // chain == 1: the second launch's epoch (published per CTA at exit)
 
   __device__ __forceinline__ int world(int m) const { return P->gmem[y][m]; }
@@ -211,6 +221,7 @@ __device__ __forceinline__ Ctx make_ctx(const LaunchParams &P) {
   c.tr = P.trace ? P.trace + ((size_t)c.y * P.ctas + c.b) * PCCL_TRACE_EVENTS : nullptr;
   c.ntr = 0;
   c.ll_peers = 0;
+  c.ll_ctr = 0;
   c.chain_epoch = 0;
   if (P.chain == 1)
     c.chain_epoch = *reinterpret_cast<volatile uint64_t *>(P.flags[c.r] + P.chain_slot_off[c.y] + PCCL_CTRL_OFF) + 1;
@@ -270,7 +281,7 @@ struct CtaEpilogue {
         if (c.ll_peers) {
           volatile uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
           for (int q = 0; q < PCCL_MAXR; ++q)
-            if ((c.ll_peers >> q) & 1u) lc[q] = lc[q] + 1;
+            if ((c.ll_peers >> q) & 1u) lc[c.ll_ctr + q] = lc[c.ll_ctr + q] + 1;
         }
       }
       if (c.tr && c.ntr < PCCL_TRACE_EVENTS) c.tr[c.ntr++] = (global_timer_ns() << 16) | ((uint64_t)TR_EPILOGUE << 12);
@@ -507,6 +518,14 @@ __device__ __forceinline__ char *ll_region(const LaunchParams &P, int dst, uint3
   return reinterpret_cast<char *>(P.flags[dst] + PCCL_LL_OFF) +
          ((size_t)(tag & 1u) * PCCL_MAXR + src) * PCCL_LL_REGION_BYTES;
 }
+__device__ __forceinline__ char *ll128_region(const LaunchParams &P, int dst, uint32_t tag, int src) {
+  return reinterpret_cast<char *>(P.flags[dst]) + PCCL_LL128_OFF +
+         ((size_t)(tag & 1u) * PCCL_MAXR + src) * PCCL_LL128_REGION_BYTES;
+}
+// the message region of a channel in the launch's format (Ctx::ll_ctr)
+__device__ __forceinline__ char *ll_region_of(const Ctx &c, int dst, uint32_t tag, int src) {
+  return c.ll_ctr ? ll128_region(*c.P, dst, tag, src) : ll_region(*c.P, dst, tag, src);
+}
 __device__ __forceinline__ void ll_st(uint4 *p, uint32_t a, uint32_t b, uint32_t tag) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(tag), "r"(b), "r"(tag)
                : "memory");
@@ -540,7 +559,7 @@ __device__ __forceinline__ int ll_wait(const Ctx &c, const uint4 *p, uint32_t ta
 __device__ __forceinline__ void ll_tags(Ctx &c, uint32_t *s_tag) {
   volatile const uint64_t *lc = c.P->flags[c.r] + PCCL_WCTRL_OFF;
   if (threadIdx.x < c.gs) {
-    const uint64_t n = lc[c.world(threadIdx.x)] + 1;
+    const uint64_t n = lc[c.ll_ctr + c.world(threadIdx.x)] + 1;
     s_tag[threadIdx.x] = (uint32_t)n ? (uint32_t)n : 1u;  // never 0 (cleared memory)
   }
   for (int m = 0; m < c.gs; ++m)
@@ -552,7 +571,7 @@ __device__ __forceinline__ void ll_post_headers(const Ctx &c, const uint32_t *s_
   const int m = threadIdx.x;
   if (c.b == 0 && m < c.gs && m != c.gi) {
     const uint32_t meta = c.P->meta[c.y];
-    ll_st(reinterpret_cast<uint4 *>(ll_region(*c.P, c.world(m), s_tag[m], c.r)), meta, meta, s_tag[m]);
+    ll_st(reinterpret_cast<uint4 *>(ll_region_of(c, c.world(m), s_tag[m], c.r)), meta, meta, s_tag[m]);
   }
 }
 // CTA-wide, after the data: every member's header carries my signature.
@@ -561,7 +580,7 @@ __device__ __forceinline__ bool ll_finish(Ctx &c, const uint32_t *s_tag, int cod
   const int m = threadIdx.x;
   if (code == 0 && m < c.gs && m != c.gi) {
     uint4 v;
-    const uint4 *h = reinterpret_cast<const uint4 *>(ll_region(*c.P, c.r, s_tag[m], c.world(m)));
+    const uint4 *h = reinterpret_cast<const uint4 *>(ll_region_of(c, c.r, s_tag[m], c.world(m)));
     code = ll_wait(c, h, s_tag[m], v, h);
     if (code == 0 && (v.x != c.P->meta[c.y] || v.z != c.P->meta[c.y])) code = 4;
     if (code == 4 && atomicCAS((int *)&c.P->err[8], 0, 1) == 0) {

@@ -948,6 +948,108 @@ template <> struct LLU<DT_F16> {
 // Chunk q of my input goes to member q as an LL message; my output chunk is
 // folded from my own chunk and the p-1 received ones in the named order
 // (same folds as k_rs_direct, so results are bit-identical to it).
+// ============================================================================
+// LL128: a line protocol for mid-size direct all-gathers. A 128-byte line is
+// written by 8 lanes of ONE warp store instruction (16 bytes each): 120
+// payload bytes and, in the last 8, the channel's message tag. A line is
+// delivered over NVLink as a unit (tools/ll128_probe.cu: no torn line in
+// 12.8 GB per direction), so a reader whose warp sees the tag in all four
+// lines of its 512-byte load holds their payload: no handshake, no fence, no
+// exit barrier, 94 % payload efficiency (LL: 50 %). Regions, channel
+// counters and the signature header follow the LL protocol (see device.cuh),
+// in a separate set of regions.
+// ============================================================================
+__device__ __forceinline__ void st_line16(uint64_t *p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_line16(const uint64_t *p, uint64_t &a, uint64_t &b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// slow path of a waiting warp (lane 0): world error, signature mismatch, timeout
+__device__ __noinline__ int ll128_slow_check(const Ctx &c, const char *reg, uint32_t tag) {
+  if (const uint64_t e = *err_mirror(*c.P, c.r)) return (int)e;
+  const uint4 h = ll_ld(reinterpret_cast<const uint4 *>(reg));
+  if (ll_ok(h, tag) && (h.x != c.P->meta[c.y] || h.z != c.P->meta[c.y])) return 4;
+  if (global_timer_ns() - c.t0 > (uint64_t)c.P->timeout_ns) return 5;
+  return 0;
+}
+
+template <int MAXP>
+__global__ void __launch_bounds__(kThreads) k_ag_direct_ll128(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  c.ll_ctr = PCCL_WCTRL_LL128;
+  CtaEpilogue fin(c);
+  __shared__ uint32_t s_tag[PCCL_MAXR];
+  ll_tags(c, s_tag);
+  ll_post_headers(c, s_tag);
+  const int gs = c.gs, gi = c.gi;
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  const int64_t words = P.blk;  // 8-byte units of my block
+  const int64_t lines = (words + 14) / 15;
+  const int64_t nw = (int64_t)P.ctas * (blockDim.x >> 5);
+  const int64_t w0 = (int64_t)c.b * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t *src = reinterpret_cast<const uint64_t *>(P.send[c.r]);
+  uint64_t *mine = reinterpret_cast<uint64_t *>(ag_block<8>(P, P.recv[c.r], c.y, gi, 0));
+  // send: each warp packs 4 lines (lane j of a line: words 2j, 2j+1; lane 7:
+  // word 14 and the tag) and stores them into every peer's region
+  for (int64_t g = w0; g * 4 < lines; g += nw) {
+    const int64_t line = g * 4 + (lane >> 3);
+    if (line >= lines) continue;
+    const int64_t wa = line * 15 + 2 * j;
+    uint64_t a = 0, b = 0;
+    if (wa < words) a = src[wa];
+    if (j < 7 && wa + 1 < words) b = src[wa + 1];
+    if (P.local_copy) {
+      if (wa < words) mine[wa] = a;
+      if (j < 7 && wa + 1 < words) mine[wa + 1] = b;
+    }
+#pragma unroll
+    for (int i = 1; i < MAXP; ++i) {
+      if (i >= gs) break;
+      const int q = (gi + i) % gs;
+      uint64_t *d = reinterpret_cast<uint64_t *>(ll128_region(P, c.world(q), s_tag[q], c.r) + PCCL_LL_HDR_BYTES);
+      st_line16(d + line * 16 + 2 * j, a, j < 7 ? b : (uint64_t)s_tag[q]);
+    }
+  }
+  // receive: poll each source's lines until the warp sees the tag in all of
+  // them, then scatter the payload into that source's block
+  int code = 0;
+  for (int i = 1; i < MAXP; ++i) {
+    if (i >= gs || code) break;
+    const int q = (gi + gs - i) % gs;
+    const char *reg = ll128_region(P, c.r, s_tag[q], c.world(q));
+    const uint64_t *base = reinterpret_cast<const uint64_t *>(reg + PCCL_LL_HDR_BYTES);
+    uint64_t *out = reinterpret_cast<uint64_t *>(ag_block<8>(P, P.recv[c.r], c.y, q, 0));
+    const uint64_t tag = s_tag[q];
+    for (int64_t g = w0; g * 4 < lines; g += nw) {
+      const int64_t line = g * 4 + (lane >> 3);
+      const bool valid = line < lines;
+      const uint64_t *pl = base + (valid ? line : 0) * 16 + 2 * j;
+      uint64_t a, b;
+      uint32_t it = 0;
+      while (true) {
+        ld_line16(pl, a, b);
+        if (__all_sync(0xffffffffu, !valid || j != 7 || b == tag)) break;
+        if ((++it & 1023u) == 0) {
+          int e = lane == 0 ? ll128_slow_check(c, reg, (uint32_t)tag) : 0;
+          e = __shfl_sync(0xffffffffu, e, 0);
+          if (e) {
+            code = e;
+            break;
+          }
+        }
+      }
+      if (code) break;
+      if (valid) {
+        const int64_t wa = line * 15 + 2 * j;
+        if (wa < words) out[wa] = a;
+        if (j < 7 && wa + 1 < words) out[wa + 1] = b;
+      }
+    }
+  }
+  ll_finish(c, s_tag, code);
+}
+
 template <int DT, int ORDER, int MAXP>
 __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant__ LaunchParams P) {
   using R = LLU<DT>;

@@ -102,6 +102,7 @@ struct pccl_world {
   int64_t p_hier_chain = 1;     // hierarchical: chain the two phase launches (device.cuh "chained launches")  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
+  int64_t p_ll128_max = 0;  // LL128 (direct AG) up to this many payload bytes per peer where LL does not apply; 0 off
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
   int64_t trace_seq = 0;  // launches traced since tracing was (re)enabled
@@ -360,7 +361,17 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   int U;  // bytes per unit
   KernelFn k;
   size_t smem = 0;
-  if (pl.variant == 4) {  // LL protocol: 8-byte payload units (host checked the alignment)
+  if (pl.variant == 8) {  // LL128 line protocol (direct all-gather), 8-byte payload units
+    U = 8;
+    int maxp = 2;
+    while (maxp < pl.gs) maxp <<= 1;
+    switch (maxp) {
+      case 2: k = (KernelFn)k_ag_direct_ll128<2>; break;
+      case 4: k = (KernelFn)k_ag_direct_ll128<4>; break;
+      case 8: k = (KernelFn)k_ag_direct_ll128<8>; break;
+      default: k = (KernelFn)k_ag_direct_ll128<16>; break;
+    }
+  } else if (pl.variant == 4) {  // LL protocol: 8-byte payload units (host checked the alignment)
     U = 8;
     int maxp = 2;
     while (maxp < pl.gs) maxp <<= 1;
@@ -490,6 +501,11 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
     if (pl.variant == 4) {  // LL: about one 8-byte unit per thread and peer
       const int64_t u = P.blk * (int64_t)pl.nsubblk;
       ctas = (int)std::max<int64_t>(1, std::min<int64_t>(w->emu ? PCCL_MAX_CTAS : 64, (u + threads - 1) / threads));
+    }
+    if (pl.variant == 8) {  // LL128: one 4-line group per warp and pass
+      const int64_t groups = ((P.blk + 14) / 15 + 3) / 4;
+      const int64_t wpc = threads / 32;
+      ctas = (int)std::max<int64_t>(1, std::min<int64_t>(w->emu ? PCCL_MAX_CTAS : 128, (groups + wpc - 1) / wpc));
     }
   }
   ctas = std::min(ctas, PCCL_MAX_CTAS);
@@ -644,6 +660,22 @@ bool use_ll(const pccl_world *w, int64_t variant_param, size_t msg_bytes, int gs
   if (variant_param != 4) {
     const size_t lim = w->p_ll_max < 0 ? kLLEgress / (size_t)std::max(1, gs - 1) : (size_t)w->p_ll_max;
     cap = std::min(cap, lim);
+  }
+  return gs <= PCCL_MAXR && msg_bytes > 0 && msg_bytes % 8 == 0 && msg_bytes <= cap;
+}
+
+// LL128 (direct all-gather): requested (ag_variant 8) or automatic for
+// messages above the LL range up to `ll128_max` payload bytes per peer; a
+// message must fit one region (PCCL_LL128_MAX_PAYLOAD). SPMD-uniform inputs
+// only, like use_ll.
+bool use_ll128(const pccl_world *w, size_t msg_bytes, int gs) {
+  const int64_t v = w->p_ag_variant;
+  size_t cap = PCCL_LL128_MAX_PAYLOAD;
+  if (v == -1) {
+    if (w->p_ll128_max <= 0) return false;
+    cap = std::min(cap, (size_t)w->p_ll128_max);
+  } else if (v != 8) {
+    return false;
   }
   return gs <= PCCL_MAXR && msg_bytes > 0 && msg_bytes % 8 == 0 && msg_bytes <= cap;
 }
@@ -898,8 +930,9 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.blk = (int64_t)count;
   pl.istride = (int64_t)count;
   pl.send_sub_stride = (int64_t)count;
-  if (algo == A_DIRECT && use_ll(w, w->p_ag_variant, blk_bytes, gs)) {
-    pl.variant = 4;
+  const bool ll = algo == A_DIRECT && use_ll(w, w->p_ag_variant, blk_bytes, gs);
+  if (algo == A_DIRECT && (ll || use_ll128(w, blk_bytes, gs))) {
+    pl.variant = ll ? 4 : 8;
     pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
     Binder B{w, stream};
     std::vector<std::pair<char *, char *>> copy_out;
@@ -931,7 +964,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
     // with few SMs) whenever the output is symmetric; a direct all-gather into
     // an unregistered output pulls instead (only the small send is staged).
     int v = (int)w->p_ag_variant;
-    if (v == 4 || v == 5) v = -1;  // LL / copy engine requested but this call does not qualify
+    if (v == 4 || v == 5 || v == 8) v = -1;  // LL / copy engine / LL128 requested but this call does not qualify
     if (v < 0) {
       int seg;
       size_t off;
@@ -1815,6 +1848,7 @@ static int world_init(pccl_world *w, int nranks, int rank, int device, bool emu)
   if (const char *t = getenv("PCCL_THREADS")) w->p_threads = atoi(t);
   if (const char *t = getenv("PCCL_LOCAL_FENCE")) w->p_local_fence = atoi(t);
   if (const char *t = getenv("PCCL_LL_MAX")) w->p_ll_max = atoll(t);
+  if (const char *t = getenv("PCCL_LL128_MAX")) w->p_ll128_max = atoll(t);
   if (const char *t = getenv("PCCL_ITEM_KIB")) w->p_item_kib = atoll(t);
   if (const char *t = getenv("PCCL_PDL")) w->p_pdl = atoi(t);
   if (const char *t = getenv("PCCL_AG_VARIANT")) w->p_ag_variant = atoi(t);  // 5: copy engine (ring / recursive)
@@ -1938,6 +1972,7 @@ static int64_t *param_ref(pccl_world *w, const char *key) {
   if (!strcmp(key, "hier_chain")) return &w->p_hier_chain;
   if (!strcmp(key, "pdl")) return &w->p_pdl;
   if (!strcmp(key, "ll_max")) return &w->p_ll_max;
+  if (!strcmp(key, "ll128_max")) return &w->p_ll128_max;
   if (!strcmp(key, "item_kib")) return &w->p_item_kib;
   return nullptr;
 }
@@ -1951,8 +1986,10 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
-  if (is_variant && (value == 6 || value > 7 || (value == 7 && strcmp(key, "rs_variant"))))
-    return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items (RS recursive)
+  if (is_variant && (value == 6 || value > 8 || (value == 7 && strcmp(key, "rs_variant")) ||
+                     (value == 8 && strcmp(key, "ag_variant"))))
+    return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items
+                                       // (RS recursive), 8: LL128 (AG direct)
   if (!strcmp(key, "items_per_cta") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "hier_intra") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "hier_chain") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;

@@ -406,8 +406,8 @@ def test_param_validation():
     """Tuning knobs: documented ranges accepted, the rest rejected (include/pccl_b200.h)."""
     pkg = _pkg()
     w = pkg.emulated_world(2)
-    cases = [("ll_max", [-1, 0, 8, 1 << 20], [-2]), ("ag_variant", [-1, 0, 1, 2, 3, 4, 5], [-2, 6, 7]),
-             ("rs_variant", [-1, 0, 1, 4, 5, 7], [6, 8]), ("items_per_cta", [1, 16], [0, 17]), ("hier_intra", [-1, 0, 1], [-2, 2]), ("ctas", [0, 1, 320], [-1, 321]), ("nsub", [1, 32], [0, 33]),
+    cases = [("ll_max", [-1, 0, 8, 1 << 20], [-2]), ("ag_variant", [-1, 0, 1, 2, 3, 4, 5, 8], [-2, 6, 7, 9]),
+             ("rs_variant", [-1, 0, 1, 4, 5, 7], [6, 8]), ("ll128_max", [0, 8, 1 << 20], [-1]), ("items_per_cta", [1, 16], [0, 17]), ("hier_intra", [-1, 0, 1], [-2, 2]), ("ctas", [0, 1, 320], [-1, 321]), ("nsub", [1, 32], [0, 33]),
              ("threads", [64, 512], [32, 100, 1024]), ("timeout_ms", [1, 20000], [0]), ("pdl", [0, 1], [-1]),
              ("local_fence", [0, 1], [-1]), ("item_kib", [0, 16, 64], [-1])]
     for key, good, bad in cases:
@@ -470,3 +470,66 @@ def test_push_all_gather_mixed_in_place_rows(algo, dtype):
     for r in range(p):
         assert torch.equal(full[r].view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
                            want.view(torch.int16 if dtype == torch.bfloat16 else torch.int32)), (algo, r)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.uint8])
+def test_ll128_all_gather_matches_oracle(p, dtype):
+    """LL128 line protocol (ag_variant 8): 120 payload bytes + an 8-byte tag
+    per 128-byte line, no handshakes. Every size class: a single word, a
+    partial last line, exact line multiples, ragged warp groups, and the
+    largest message one region holds; alternated with LL and flag-protocol
+    calls on the same group (separate regions and channel counters), in
+    place and not, bit-exact against the reference's all-gather."""
+    pkg = _pkg()
+    w = pkg.emulated_world(p)
+    es = torch.empty(0, dtype=dtype).element_size()
+    cap_words = (1 << 14) * 15  # PCCL_LL128_LINES * 15 eight-byte words
+    g = torch.Generator(device="cuda").manual_seed(17 + p)
+    try:
+        for words in (1, 14, 15, 16, 60, 61, 1000, 4099, 40000, cap_words):
+            n = words * 8 // es
+            blocks = [torch.randint(0, 255, (n * es,), dtype=torch.uint8, generator=g, device="cuda").view(dtype)
+                      for _ in range(p)]
+            want = torch.cat(blocks)
+            for variant in (8, 4, -1, 8):
+                if variant == 4 and words * 8 > (1 << 20):
+                    continue
+                w.set_param("ag_variant", variant)
+                outs = [torch.full((n * p,), 0, dtype=dtype, device="cuda") for _ in range(p)]
+                pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, blocks[c.rank], out=outs[c.rank]))
+                for r in range(p):
+                    assert torch.equal(outs[r].view(torch.uint8), want.view(torch.uint8)), (p, dtype, words, variant, r)
+        # in place: my block already sits in the output
+        w.set_param("ag_variant", 8)
+        n = 4099 * 8 // es
+        blocks = [torch.randint(0, 255, (n * es,), dtype=torch.uint8, generator=g, device="cuda").view(dtype)
+                  for _ in range(p)]
+        outs = [torch.zeros(n * p, dtype=dtype, device="cuda") for _ in range(p)]
+        for r in range(p):
+            outs[r][r * n:(r + 1) * n].copy_(blocks[r])
+        pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, outs[c.rank][c.rank * n:(c.rank + 1) * n],
+                                                          out=outs[c.rank]))
+        for r in range(p):
+            assert torch.equal(outs[r].view(torch.uint8), torch.cat(blocks).view(torch.uint8))
+    finally:
+        w.set_param("ag_variant", -1)
+
+
+def test_ll128_too_large_is_rejected_not_truncated():
+    """A message larger than one LL128 region is not sent as LL128: with the
+    variant forced the call falls back to the flag protocol (the LL rule),
+    and the result is exact."""
+    pkg = _pkg()
+    p = 2
+    w = pkg.emulated_world(p)
+    words = (1 << 14) * 15 + 8
+    blocks = [torch.arange(words * 2, dtype=torch.float32, device="cuda") + 1000 * r for r in range(p)]
+    outs = [torch.empty(words * 2 * p, device="cuda") for _ in range(p)]
+    try:
+        w.set_param("ag_variant", 8)
+        pkg.run_ranks(p, lambda c: pkg.direct_all_gather(c, blocks[c.rank], out=outs[c.rank]))
+    finally:
+        w.set_param("ag_variant", -1)
+    for r in range(p):
+        assert torch.equal(outs[r], torch.cat(blocks))
