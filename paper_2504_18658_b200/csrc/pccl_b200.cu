@@ -102,7 +102,10 @@ struct pccl_world {
   int64_t p_hier_chain = 1;     // hierarchical: chain the two phase launches (device.cuh "chained launches")  // direct kernels: dynamically claimed work items of this size (0: static CTA slices)
   int64_t p_staged_bytes = 0;  // statistic: bytes of caller buffers bound through staging (get_param; set 0 = reset)
   int64_t p_ll_max = -1;  // LL protocol up to this many payload bytes per peer; 0 off, -1 auto (kLLEgress / (gs-1))
-  int64_t p_ll128_max = 0;  // LL128 (direct AG) up to this many payload bytes per peer where LL does not apply; 0 off
+  // LL128 (direct AG) up to this many payload bytes per peer where LL does not
+  // apply; 0 off. Default: whatever one region holds (tools/tune.py, p=2/4,
+  // 1-7 MiB: never slower than the flag protocol, up to 1.7x at p=2 / 3 MiB)
+  int64_t p_ll128_max = (int64_t)PCCL_LL128_MAX_PAYLOAD;
   uint64_t *trace_buf = nullptr;  // device, PCCL_MAXR x PCCL_MAX_CTAS x PCCL_TRACE_EVENTS
   int trace_rows = 0, trace_ctas = 0;
   int64_t trace_seq = 0;  // launches traced since tracing was (re)enabled

@@ -106,7 +106,7 @@ def main() -> int:
         # 5: copy engine (ring / recursive into a registered output; every rank
         # takes the same choice, a call that does not qualify is an error)
         use_ce = ce and coll == "ag" and kind == "sym" and algo != "direct" and rng.random() < 0.4
-        w.set_param("ag_variant", 5 if use_ce else -1)
+        w.set_param("ag_variant", 5 if use_ce else (8 if coll == "ag" and rng.random() < 0.3 else -1))
         total_in = n if coll == "ag" else n * p
         total_out = n * p if coll == "ag" else n
         if kind == "sym":

@@ -124,6 +124,17 @@ def main() -> int:
               oracle.direct_reduce_scatter(bf, "bf16", "ring")[rank])
     comm.world.set_param("rs_variant", -1)
     sync_point("rs_pipelined_push")
+    # LL128 line protocol (ag_variant 8) over real NVLink: sizes from one word
+    # to a full region, alternated with LL and flag-protocol calls
+    for words in (1, 15, 61, 4099, 100_000, (1 << 14) * 15):
+        ag_in = [rng.standard_normal(words * 2).astype(np.float32) for _ in range(p)]
+        want = oracle.ring_all_gather(ag_in)[rank]
+        for variant in (8, -1, 8):
+            comm.world.set_param("ag_variant", variant)
+            got = pkg.direct_all_gather(comm, torch.from_numpy(ag_in[rank]).cuda())
+            check(f"ll128_v{variant}_w{words}", got.cpu().numpy(), want)
+    comm.world.set_param("ag_variant", -1)
+    sync_point("ll128")
     # NVLS multicast segment (switch-executed AG stores / RS loads)
     from paper_2504_18658_b200 import nvls as NV
 

@@ -234,7 +234,8 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
     try:
         w.set_param("trace", 1)
         w.set_param("nsub", 1)
-        w.set_param("ll_max", 0)  # the bulk (flag) protocol: LL has no per-step waits
+        w.set_param("ll_max", 0)  # the bulk (flag) protocol: LL / LL128 have no per-step waits
+        w.set_param("ll128_max", 0)
         s = torch.cuda.current_stream().cuda_stream
         if coll == "rs":
             _lib.check(L.pccl_emu_reduce_scatter(group.handle, a, 0, sp, rp, n, 0, s))
@@ -245,6 +246,7 @@ def test_device_step_structure_matches_schedule(p, coll, algo):
     finally:
         w.set_param("trace", 0)
         w.set_param("ll_max", ll_max)
+        w.set_param("ll128_max", 1 << 30)  # back to "whatever a region holds"
     assert len(tr) == p
     # default data movement for symmetric buffers: AG push, RS pull. Waits
     # per CTA = the algorithm's steps plus the push handshakes ("your buffer

@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=100000, help="collectives per (local_fence) setting")
     ap.add_argument("--fences", default="1,0")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--movement", choices=["pull", "default"], default="pull",
+    ap.add_argument("--movement", choices=["pull", "default", "ll128"], default="pull",
                     help="pull: force pull kernels (the local_fence publish); default: the library's choice")
     a = ap.parse_args()
     rank, p = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -45,6 +45,10 @@ def main():
     if a.movement == "pull":
         w.set_param("rs_variant", 0)    # pull
         w.set_param("ag_variant", 0)    # pull
+    if a.movement != "ll128":
+        w.set_param("ll128_max", 0)     # flag protocol only
+    if a.movement == "ll128":
+        w.set_param("ag_variant", 8)    # LL128 line protocol for every direct all-gather that fits a region
     # "default": the library's choice for symmetric buffers (RS pull, AG push
     # with the rank-level final publish)
     stream = torch.cuda.current_stream(dev).cuda_stream
