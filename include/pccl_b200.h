@@ -112,11 +112,15 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
  * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
  * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL, 5 copy engine (AG ring /
  * recursive doubling, see pccl_ce_available) / pipelined push with pusher and folder CTAs (RS
- * direct)), "tma_stages",
+ * direct), 7 work items (RS recursive), 8 LL128 (AG direct)), "tma_stages",
  * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
  * collectives use the LL protocol — flags inside 16-byte data words, no
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
- * (group size - 1), 0 off), "item_kib" (direct collectives: CTAs claim work
+ * (group size - 1), 0 off), "ll128_max" (direct all-gathers the LL rule does
+ * not take use the LL128 line protocol — 120 payload bytes + a tag per
+ * 128-byte line written by one warp instruction — up to this many payload
+ * bytes per peer, capped at one region (1.875 MiB); default: the cap, 0 off),
+ * "item_kib" (direct collectives: CTAs claim work
  * items of this many KiB from a device counter instead of static slices;
  * default 0 = static; measured: no gain, see DESIGN), "staged_bytes" (statistic:
  * bytes of caller buffers that went through staging because they were not in a
@@ -124,7 +128,8 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
 int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value);
 int pccl_world_get_param(pccl_world_t w, const char *key, int64_t *value);
 /* With param "trace" = 1, every launch records per-CTA events (globaltimer ns
- * << 16 | kind << 12 | unit; kind 1 start, 2 wait done, 3 signal, 4 end),
+ * << 16 | kind << 12 | unit; kind 1 start, 2 wait done, 3 signal, 4 end, 5 exit,
+ * 6 resident (before the PDL wait), 7 after the exit counter, 8 PDL release),
  * 128 words per CTA, laid out [row][cta][event]; copies the last launch's. */
 int pccl_world_trace(pccl_world_t w, uint64_t *host, size_t cap_words, int *rows, int *ctas);
 /* Param "trace" = K (2..8): the last K launches are kept; back = 0 is the
