@@ -112,14 +112,15 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
  * CTA, 64..512), "nsub" (pipeline sub-slices), "ag_variant" / "rs_variant" (data movement: -1 auto, 0 pull = LDG
  * from peers, 1 push = STG into peers, 2 TMA pull, 3 TMA push, 4 LL, 5 copy engine (AG ring /
  * recursive doubling, see pccl_ce_available) / pipelined push with pusher and folder CTAs (RS
- * direct), 7 work items (RS recursive), 8 LL128 (AG direct)), "tma_stages",
+ * direct), 7 work items (RS recursive), 8 LL128 (direct)), "tma_stages",
  * "tma_tile", "timeout_ms", "trace", "local_fence", "pdl", "ll_max" (direct
  * collectives use the LL protocol — flags inside 16-byte data words, no
  * handshakes — up to this many payload bytes per peer; -1 auto = 768 KiB /
- * (group size - 1), 0 off), "ll128_max" (direct all-gathers the LL rule does
+ * (group size - 1), 0 off), "ll128_max" (direct collectives the LL rule does
  * not take use the LL128 line protocol — 120 payload bytes + a tag per
  * 128-byte line written by one warp instruction — up to this many payload
- * bytes per peer, capped at one region (1.875 MiB); default: the cap, 0 off),
+ * bytes per peer, capped at one region (1.875 MiB) and, for reduce-scatters,
+ * at 3 MiB / (group size - 1); default: the cap, 0 off),
  * "item_kib" (direct collectives: CTAs claim work
  * items of this many KiB from a device counter instead of static slices;
  * default 0 = static; measured: no gain, see DESIGN), "staged_bytes" (statistic:

@@ -945,9 +945,6 @@ template <> struct LLU<DT_F16> {
   }
 };
 
-// Chunk q of my input goes to member q as an LL message; my output chunk is
-// folded from my own chunk and the p-1 received ones in the named order
-// (same folds as k_rs_direct, so results are bit-identical to it).
 // ============================================================================
 // LL128: a line protocol for mid-size direct all-gathers. A 128-byte line is
 // written by 8 lanes of ONE warp store instruction (16 bytes each): 120
@@ -1050,6 +1047,9 @@ __global__ void __launch_bounds__(kThreads) k_ag_direct_ll128(const __grid_const
   ll_finish(c, s_tag, code);
 }
 
+// Chunk q of my input goes to member q as an LL message; my output chunk is
+// folded from my own chunk and the p-1 received ones in the named order
+// (same folds as k_rs_direct, so results are bit-identical to it).
 template <int DT, int ORDER, int MAXP>
 __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant__ LaunchParams P) {
   using R = LLU<DT>;
@@ -1142,6 +1142,133 @@ __global__ void __launch_bounds__(kThreads) k_rs_direct_ll(const __grid_constant
           }
       }
       dst[e] = R::store(acc);
+    }
+  }
+  ll_finish(c, s_tag, code);
+}
+
+// Fold of the p values of one 8-byte unit in the named order (fold position
+// i holds member q: ring q = gi + 1 + i, butterfly q = gi ^ i, rank q = i),
+// rounding every partial to the storage type when `wire` — the same
+// arithmetic as k_rs_direct_ll, so LL128 and LL results are bit-identical.
+template <int DT, int ORDER, int MAXP>
+__device__ __forceinline__ uint64_t ll_fold(const uint64_t (&u)[MAXP], int gs, int wire) {
+  using R = LLU<DT>;
+  using Acc = typename R::Acc;
+  auto ld = [](uint64_t x) { return R::load(make_uint2((uint32_t)x, (uint32_t)(x >> 32))); };
+  Acc acc;
+  if (ORDER == O_REC) {
+    Acc v[MAXP];
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i) v[i] = ld(u[i]);
+#pragma unroll
+    for (int h = MAXP / 2; h >= 1; h >>= 1) {
+      if (h < gs) {
+#pragma unroll
+        for (int m = 0; m < h; ++m) {
+          acc_add<Acc, R::N>(v[m], v[m ^ h]);
+          if (DT != DT_F32 && wire) v[m] = R::load(R::store(v[m]));
+        }
+      }
+    }
+    acc = v[0];
+  } else if (ORDER == O_RANK) {
+#pragma unroll
+    for (int k = 0; k < R::N; ++k) acc.v[k] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i)
+      if (i < gs) acc_add<Acc, R::N>(acc, ld(u[i]));
+  } else {
+    acc = ld(u[0]);
+#pragma unroll
+    for (int i = 1; i < MAXP; ++i)
+      if (i < gs) {
+        acc_add<Acc, R::N>(acc, ld(u[i]));
+        if (DT != DT_F32 && wire) acc = R::load(R::store(acc));
+      }
+  }
+  const uint2 o = R::store(acc);
+  return (uint64_t)o.x | ((uint64_t)o.y << 32);
+}
+
+// LL128 reduce-scatter: chunk q of my input goes to member q as LL128 lines;
+// my output is folded from my own chunk and the p - 1 received line streams
+// (a warp waits until all four lines of a group carry the tag, per source).
+template <int DT, int ORDER, int MAXP>
+__global__ void __launch_bounds__(kThreads) k_rs_direct_ll128(const __grid_constant__ LaunchParams P) {
+  Ctx c = make_ctx(P);
+  c.ll_ctr = PCCL_WCTRL_LL128;
+  CtaEpilogue fin(c);
+  __shared__ uint32_t s_tag[PCCL_MAXR];
+  ll_tags(c, s_tag);
+  ll_post_headers(c, s_tag);
+  const int gs = c.gs, gi = c.gi;
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  const int64_t words = P.blk;  // 8-byte units of one chunk
+  const int64_t lines = (words + 14) / 15;
+  const int64_t nw = (int64_t)P.ctas * (blockDim.x >> 5);
+  const int64_t w0 = (int64_t)c.b * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t *own = reinterpret_cast<const uint64_t *>(P.send[c.r]) + P.base[c.y];
+  for (int64_t g = w0; g * 4 < lines; g += nw) {
+    const int64_t line = g * 4 + (lane >> 3);
+    if (line >= lines) continue;
+    const int64_t wa = line * 15 + 2 * j;
+#pragma unroll
+    for (int i = 1; i < MAXP; ++i) {
+      if (i >= gs) break;
+      const int q = (gi + i) % gs;
+      const uint64_t *src = own + (int64_t)q * P.istride;
+      const uint64_t a = wa < words ? src[wa] : 0ull;
+      const uint64_t b = (j < 7 && wa + 1 < words) ? src[wa + 1] : (uint64_t)s_tag[q];
+      uint64_t *d = reinterpret_cast<uint64_t *>(ll128_region(P, c.world(q), s_tag[q], c.r) + PCCL_LL_HDR_BYTES);
+      st_line16(d + line * 16 + 2 * j, a, j < 7 ? b : (uint64_t)s_tag[q]);
+    }
+  }
+  uint64_t *dst = reinterpret_cast<uint64_t *>(P.out[c.r]);
+  const uint64_t *mine = own + (int64_t)gi * P.istride;
+  int code = 0;
+  for (int64_t g = w0; g * 4 < lines; g += nw) {
+    const int64_t line = g * 4 + (lane >> 3);
+    const bool valid = line < lines;
+    const int64_t wa = line * 15 + 2 * j;
+    uint64_t va[MAXP], vb[MAXP];
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i) {
+      va[i] = vb[i] = 0ull;
+      if (i >= gs || code) continue;
+      int q;
+      if (ORDER == O_RING) q = (gi + 1 + i) % gs;
+      else if (ORDER == O_REC) q = gi ^ i;
+      else q = i;
+      if (q == gi) {
+        if (valid && wa < words) va[i] = mine[wa];
+        if (valid && j < 7 && wa + 1 < words) vb[i] = mine[wa + 1];
+        continue;
+      }
+      const char *reg = ll128_region(P, c.r, s_tag[q], c.world(q));
+      const uint64_t *pl = reinterpret_cast<const uint64_t *>(reg + PCCL_LL_HDR_BYTES) + (valid ? line : 0) * 16 + 2 * j;
+      const uint64_t tag = s_tag[q];
+      uint64_t a, b;
+      uint32_t it = 0;
+      while (true) {
+        ld_line16(pl, a, b);
+        if (__all_sync(0xffffffffu, !valid || j != 7 || b == tag)) break;
+        if ((++it & 1023u) == 0) {
+          int e = lane == 0 ? ll128_slow_check(c, reg, (uint32_t)tag) : 0;
+          e = __shfl_sync(0xffffffffu, e, 0);
+          if (e) {
+            code = e;
+            break;
+          }
+        }
+      }
+      va[i] = a;
+      vb[i] = j < 7 ? b : 0ull;
+    }
+    if (code) break;
+    if (valid) {
+      if (wa < words) dst[wa] = ll_fold<DT, ORDER, MAXP>(va, gs, P.wire);
+      if (j < 7 && wa + 1 < words) dst[wa + 1] = ll_fold<DT, ORDER, MAXP>(vb, gs, P.wire);
     }
   }
   ll_finish(c, s_tag, code);

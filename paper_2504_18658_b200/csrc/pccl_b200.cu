@@ -281,6 +281,29 @@ KernelFn rs_ll_dt(int order, int maxp) {
 #undef RLL
   return nullptr;
 }
+template <int DT>
+KernelFn rs_ll128_dt(int order, int maxp) {
+#define RLL(O)                                                    \
+  if (order == O) {                                               \
+    switch (maxp) {                                               \
+      case 2: return (KernelFn)k_rs_direct_ll128<DT, O, 2>;       \
+      case 4: return (KernelFn)k_rs_direct_ll128<DT, O, 4>;       \
+      case 8: return (KernelFn)k_rs_direct_ll128<DT, O, 8>;       \
+      default: return (KernelFn)k_rs_direct_ll128<DT, O, 16>;     \
+    }                                                             \
+  }
+  RLL(O_RING)
+  RLL(O_REC)
+  RLL(O_RANK)
+#undef RLL
+  return nullptr;
+}
+KernelFn rs_ll128_kernel(int dt, int order, int maxp) {
+  if (dt == PCCL_FLOAT32) return rs_ll128_dt<DT_F32>(order, maxp);
+  if (dt == PCCL_BFLOAT16) return rs_ll128_dt<DT_BF16>(order, maxp);
+  if (dt == PCCL_FLOAT16) return rs_ll128_dt<DT_F16>(order, maxp);
+  return nullptr;
+}
 KernelFn rs_ll_kernel(int dt, int order, int maxp) {
   if (dt == PCCL_FLOAT32) return rs_ll_dt<DT_F32>(order, maxp);
   if (dt == PCCL_BFLOAT16) return rs_ll_dt<DT_BF16>(order, maxp);
@@ -364,15 +387,19 @@ int launch(pccl_world *w, Plan &pl, cudaStream_t stream) {
   int U;  // bytes per unit
   KernelFn k;
   size_t smem = 0;
-  if (pl.variant == 8) {  // LL128 line protocol (direct all-gather), 8-byte payload units
+  if (pl.variant == 8) {  // LL128 line protocol (direct collectives), 8-byte payload units
     U = 8;
     int maxp = 2;
     while (maxp < pl.gs) maxp <<= 1;
-    switch (maxp) {
-      case 2: k = (KernelFn)k_ag_direct_ll128<2>; break;
-      case 4: k = (KernelFn)k_ag_direct_ll128<4>; break;
-      case 8: k = (KernelFn)k_ag_direct_ll128<8>; break;
-      default: k = (KernelFn)k_ag_direct_ll128<16>; break;
+    if (pl.coll == PCCL_ALL_GATHER) {
+      switch (maxp) {
+        case 2: k = (KernelFn)k_ag_direct_ll128<2>; break;
+        case 4: k = (KernelFn)k_ag_direct_ll128<4>; break;
+        case 8: k = (KernelFn)k_ag_direct_ll128<8>; break;
+        default: k = (KernelFn)k_ag_direct_ll128<16>; break;
+      }
+    } else {
+      k = rs_ll128_kernel(pl.dtype, pl.order, maxp);
     }
   } else if (pl.variant == 4) {  // LL protocol: 8-byte payload units (host checked the alignment)
     U = 8;
@@ -667,16 +694,21 @@ bool use_ll(const pccl_world *w, int64_t variant_param, size_t msg_bytes, int gs
   return gs <= PCCL_MAXR && msg_bytes > 0 && msg_bytes % 8 == 0 && msg_bytes <= cap;
 }
 
-// LL128 (direct all-gather): requested (ag_variant 8) or automatic for
+// LL128 (direct collectives): requested (variant 8) or automatic for
 // messages above the LL range up to `ll128_max` payload bytes per peer; a
 // message must fit one region (PCCL_LL128_MAX_PAYLOAD). SPMD-uniform inputs
 // only, like use_ll.
-bool use_ll128(const pccl_world *w, size_t msg_bytes, int gs) {
-  const int64_t v = w->p_ag_variant;
+// A reduce-scatter's owner folds p - 1 line streams: measured (tools/tune.py,
+// bf16) it wins up to ~3 MiB of egress per rank (p=4: 1 MiB per peer +2..10 %,
+// 1.25 MiB -4 %; p=2 up to the region, +23..31 %), so its automatic range is
+// also capped by kLL128RsEgress / (p - 1). All-gathers win up to the region.
+constexpr size_t kLL128RsEgress = (size_t)3 << 20;
+bool use_ll128(const pccl_world *w, int64_t v, size_t msg_bytes, int gs, bool reduce) {
   size_t cap = PCCL_LL128_MAX_PAYLOAD;
   if (v == -1) {
     if (w->p_ll128_max <= 0) return false;
     cap = std::min(cap, (size_t)w->p_ll128_max);
+    if (reduce) cap = std::min(cap, kLL128RsEgress / (size_t)std::max(1, gs - 1));
   } else if (v != 8) {
     return false;
   }
@@ -934,7 +966,7 @@ int do_all_gather(pccl_comm *c, int algo, const std::vector<int> &ranks, const v
   pl.istride = (int64_t)count;
   pl.send_sub_stride = (int64_t)count;
   const bool ll = algo == A_DIRECT && use_ll(w, w->p_ag_variant, blk_bytes, gs);
-  if (algo == A_DIRECT && (ll || use_ll128(w, blk_bytes, gs))) {
+  if (algo == A_DIRECT && (ll || use_ll128(w, w->p_ag_variant, blk_bytes, gs, false))) {
     pl.variant = ll ? 4 : 8;
     pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
     Binder B{w, stream};
@@ -1049,8 +1081,9 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
   pl.blk = (int64_t)recvcount;
   pl.istride = (int64_t)recvcount;
   pl.out_sub_stride = (int64_t)recvcount;
-  if (algo == A_DIRECT && use_ll(w, w->p_rs_variant, chunk_bytes, gs)) {
-    pl.variant = 4;
+  const bool ll = algo == A_DIRECT && use_ll(w, w->p_rs_variant, chunk_bytes, gs);
+  if (algo == A_DIRECT && (ll || use_ll128(w, w->p_rs_variant, chunk_bytes, gs, true))) {
+    pl.variant = ll ? 4 : 8;
     pl.local_copy = 0;  // OR over the rows below: one value per launch, a self-copy is harmless
     Binder B{w, stream};
     std::vector<std::pair<char *, char *>> copy_out;
@@ -1080,7 +1113,7 @@ int do_reduce_scatter(pccl_comm *c, int algo, int order, const std::vector<int> 
     // pull ring measured 580 vs 502 GB/s at p=2 and 597 vs 583 at p=4
     // (128 MiB bf16, profiles/r2_rs_ring_pull_vs_push.txt).
     int v = (int)w->p_rs_variant;
-    if (v == 4) v = -1;  // LL requested but this message does not qualify
+    if (v == 4 || v == 8) v = -1;  // LL / LL128 requested but this message does not qualify
     if (v < 0) {
       int seg;
       size_t off;
@@ -1989,10 +2022,9 @@ int pccl_world_set_param(pccl_world_t w, const char *key, int64_t value) {
   if (!strcmp(key, "ctas") && value > PCCL_MAX_CTAS) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "nsub") && (value < 1 || value > 32)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "threads") && (value < 64 || value > kThreads || value % 32)) return PCCL_ERR_INVALID_ARGUMENT;
-  if (is_variant && (value == 6 || value > 8 || (value == 7 && strcmp(key, "rs_variant")) ||
-                     (value == 8 && strcmp(key, "ag_variant"))))
+  if (is_variant && (value == 6 || value > 8 || (value == 7 && strcmp(key, "rs_variant"))))
     return PCCL_ERR_INVALID_ARGUMENT;  // 4 LL, 5: copy engine (AG) / pipelined push (RS direct), 7: work items
-                                       // (RS recursive), 8: LL128 (AG direct)
+                                       // (RS recursive), 8: LL128 (direct)
   if (!strcmp(key, "items_per_cta") && (value < 1 || value > 16)) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "hier_intra") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;
   if (!strcmp(key, "hier_chain") && value > 1) return PCCL_ERR_INVALID_ARGUMENT;

@@ -97,7 +97,7 @@ def main() -> int:
         order = rng.choice(["ring", "rank"] + (["recursive"] if pow2 else []))
         kind = rng.choice(["sym", "plain", "misaligned", "host"] if coll != "hier" else ["sym", "plain", "misaligned"])
         w.set_param("item_kib", rng.choice([0, 0, 16, 64]))  # direct kernels: static slices / work items
-        w.set_param("rs_variant", rng.choice([-1, -1, 5, 7]))  # 5: pipelined push (direct), 7: work items (recursive)
+        w.set_param("rs_variant", rng.choice([-1, -1, 5, 7, 8]))  # 5: pipelined push (direct), 7: work items (recursive), 8: LL128
         # hierarchical: intra phase auto / ring / direct, chained or separate
         # phase launches, CTA count default or forced (chaining needs <= 128)
         w.set_param("hier_intra", rng.choice([-1, 0, 1]))

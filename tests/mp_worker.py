@@ -134,6 +134,16 @@ def main() -> int:
             got = pkg.direct_all_gather(comm, torch.from_numpy(ag_in[rank]).cuda())
             check(f"ll128_v{variant}_w{words}", got.cpu().numpy(), want)
     comm.world.set_param("ag_variant", -1)
+    # LL128 reduce-scatter: the direct fold in every order over line streams
+    for words in (1, 61, 4099, (1 << 14) * 15):
+        rs_in = [rng.standard_normal(words * 2 * p).astype(np.float32) for _ in range(p)]
+        for order in ["ring", "rank"] + (["recursive"] if pow2 else []):
+            want = oracle.direct_reduce_scatter(rs_in, "f32", order)[rank]
+            for variant in (8, -1):
+                comm.world.set_param("rs_variant", variant)
+                got = pkg.direct_reduce_scatter(comm, torch.from_numpy(rs_in[rank]).cuda(), order=order)
+                check(f"ll128_rs_{order}_v{variant}_w{words}", got.cpu().numpy(), want)
+    comm.world.set_param("rs_variant", -1)
     sync_point("ll128")
     # NVLS multicast segment (switch-executed AG stores / RS loads)
     from paper_2504_18658_b200 import nvls as NV

@@ -169,6 +169,36 @@ def test_ll128_all_gather_writes_only_its_output(kind, p, words):
         w.set_param("ag_variant", -1)
 
 
+@pytest.mark.parametrize("kind", ["sym", "plain", "misaligned"])
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("words", [1, 61, 70000])
+def test_ll128_reduce_scatter_writes_only_its_output(kind, p, words):
+    """LL128 reduce-scatter: no write past the output chunk (padding of the
+    last line), guards of inputs / outputs intact, result equal to the
+    oracle's direct ring-order fold."""
+    pkg = _pkg()
+    from paper_2504_18658_b200.communicator import emulated_world
+
+    w = emulated_world(p, 0)
+    n = words * 2
+    rng = np.random.default_rng(words * 7 + p)
+    ins = [rng.standard_normal(n * p).astype(np.float32) for _ in range(p)]
+    w.set_param("rs_variant", 8)
+    try:
+        xs, x_ok = _guarded(n * p, torch.float32, kind, w)
+        ys, y_ok = _guarded(n, torch.float32, kind, w)
+        for r in range(p):
+            xs[r].copy_(torch.from_numpy(ins[r]))
+        pkg.run_ranks(p, lambda c: pkg.direct_reduce_scatter(c, xs[c.rank], order="ring", out=ys[c.rank]))
+        torch.cuda.synchronize()
+        assert x_ok() and y_ok(), (kind, p, words)
+        want = oracle.direct_reduce_scatter(ins, "f32", order="ring")
+        for r in range(p):
+            assert np.array_equal(_bits(ys[r]).view(np.uint32), np.asarray(want[r]).view(np.uint32)), (kind, p, words, r)
+    finally:
+        w.set_param("rs_variant", -1)
+
+
 @pytest.mark.parametrize("variant", [0, 1, 5])
 @pytest.mark.parametrize("n", [3, 4099, 70001])
 def test_reduce_scatter_variants_write_only_their_output(variant, n):

@@ -48,7 +48,8 @@ def main():
     if a.movement != "ll128":
         w.set_param("ll128_max", 0)     # flag protocol only
     if a.movement == "ll128":
-        w.set_param("ag_variant", 8)    # LL128 line protocol for every direct all-gather that fits a region
+        w.set_param("ag_variant", 8)    # LL128 line protocol for every direct collective that fits a region
+        w.set_param("rs_variant", 8)
     # "default": the library's choice for symmetric buffers (RS pull, AG push
     # with the rank-level final publish)
     stream = torch.cuda.current_stream(dev).cuda_stream
