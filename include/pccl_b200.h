@@ -119,8 +119,8 @@ int pccl_world_set_timeout_ms(pccl_world_t w, int64_t ms);
  * (group size - 1), 0 off), "ll128_max" (direct collectives the LL rule does
  * not take use the LL128 line protocol — 120 payload bytes + a tag per
  * 128-byte line written by one warp instruction — up to this many payload
- * bytes per peer, capped at one region (1.875 MiB) and, for reduce-scatters,
- * at 3 MiB / (group size - 1); default: the cap, 0 off),
+ * bytes per peer, capped at one region (1.875 MiB) and at 6 MiB (all-gather) /
+ * 3 MiB (reduce-scatter) / (group size - 1); default: the cap, 0 off),
  * "item_kib" (direct collectives: CTAs claim work
  * items of this many KiB from a device counter instead of static slices;
  * default 0 = static; measured: no gain, see DESIGN), "staged_bytes" (statistic:

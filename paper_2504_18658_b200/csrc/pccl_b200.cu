@@ -701,14 +701,17 @@ bool use_ll(const pccl_world *w, int64_t variant_param, size_t msg_bytes, int gs
 // A reduce-scatter's owner folds p - 1 line streams: measured (tools/tune.py,
 // bf16) it wins up to ~3 MiB of egress per rank (p=4: 1 MiB per peer +2..10 %,
 // 1.25 MiB -4 %; p=2 up to the region, +23..31 %), so its automatic range is
-// also capped by kLL128RsEgress / (p - 1). All-gathers win up to the region.
+// also capped by kLL128RsEgress / (p - 1). All-gathers were measured up to
+// 5.25 MiB of egress (p=4, 7 MiB: +4 %); beyond that (p=8 with full regions)
+// they are capped at kLL128AgEgress / (p - 1), unmeasured above.
 constexpr size_t kLL128RsEgress = (size_t)3 << 20;
+constexpr size_t kLL128AgEgress = (size_t)6 << 20;
 bool use_ll128(const pccl_world *w, int64_t v, size_t msg_bytes, int gs, bool reduce) {
   size_t cap = PCCL_LL128_MAX_PAYLOAD;
   if (v == -1) {
     if (w->p_ll128_max <= 0) return false;
     cap = std::min(cap, (size_t)w->p_ll128_max);
-    if (reduce) cap = std::min(cap, kLL128RsEgress / (size_t)std::max(1, gs - 1));
+    cap = std::min(cap, (reduce ? kLL128RsEgress : kLL128AgEgress) / (size_t)std::max(1, gs - 1));
   } else if (v != 8) {
     return false;
   }
